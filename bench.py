@@ -1,0 +1,498 @@
+#!/usr/bin/env python
+"""Benchmark of the ISAAC render hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config c4]
+
+One JSON line on rank 0.  A "step" is one frame: ``render_local`` of this
+rank's brick (the sm_100a march kernel) + ``binary_swap`` of the sub-images
+(the fused peer-memory swap kernel; a device copy at N=1).  Default workload
+(N=1 and every N): config C4 of BASELINE.json -- a 1024^3 float32 field with
+a one-cell guard, decomposed into N bricks (1x1x1, 2x1x1, 2x2x1, 2x2x2; strong
+scaling), rendered at 1920x1080 with the reference harness camera, trilinear
+sampling, step 0.5, linear transfer function, early termination off.
+
+Under torchrun each rank drives one GPU.  Timing: W untimed steps, then K
+steps bracketed by barrier + synchronize, CUDA events on the launching
+stream, max over ranks.  The 4.32 GB field is far larger than the 126 MB L2,
+so no explicit L2 flush is needed between steps (stated in ``config``).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "frames/sec and Gsamples/sec at 1024³×1080p, 1/2/4/8 B200; % of HBM roofline"
+DECOMP = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2), 16: (4, 2, 2)}
+CONFIGS = {
+    "c4": dict(n=1024, image=(1920, 1080), desc="1024^3 float32 field (1 cell guard), 1920x1080, trilinear, "
+                                                "linear TF, harness camera, step 0.5, bricks across N GPUs"),
+    "c2": dict(n=512, image=(1920, 1080), clip=True, desc="512^3 float32, 1920x1080, trilinear + clip plane"),
+    "c1": dict(n=64, image=(256, 256), desc="64^3 float32, 256x256, trilinear, linear TF"),
+}
+BYTES_PER_SAMPLE = 32       # 8 trilinear corners x 4 B
+BYTES_PER_PIXEL_OUT = 16    # float32 RGBA written per pixel
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def peak_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def harness_camera(n):
+    diag = math.sqrt(3.0 * n * n)
+    return (n * 1.4, n * 1.15, -0.8 * diag), (n / 2.0, n / 2.0, n / 2.0)
+
+
+def field_terms(n):
+    """Separable smooth field f = 1 + sin(0.4 x s) cos(0.3 y s) + 0.4 sin(0.5 z s), s = 64/n
+    (scaled from test_raycast.py:230-231); range ~[-0.4, 2.4]."""
+    s = 64.0 / n
+    return (lambda x: math.sin(0.4 * x * s)), (lambda y: math.cos(0.3 * y * s)), (lambda z: 0.4 * math.sin(0.5 * z * s))
+
+
+def make_field_torch(n, domain, device, dtype=None):
+    import torch
+    g = domain.guard_width
+    ox, oy, oz = domain.offset
+    sx, sy, sz = domain.size
+    s = 64.0 / n
+    dt = torch.float64
+    x = torch.arange(ox - g, ox + sx + g, dtype=dt, device=device)
+    y = torch.arange(oy - g, oy + sy + g, dtype=dt, device=device)
+    z = torch.arange(oz - g, oz + sz + g, dtype=dt, device=device)
+    ab = (1.0 + torch.sin(0.4 * x * s)[None, :] * torch.cos(0.3 * y * s)[:, None]).float()
+    cz = (0.4 * torch.sin(0.5 * z * s)).float()
+    out = torch.empty((sz + 2 * g, sy + 2 * g, sx + 2 * g), dtype=torch.float32, device=device)
+    for z0 in range(0, out.shape[0], 64):
+        out[z0:z0 + 64] = ab[None] + cz[z0:z0 + 64, None, None]
+    return out
+
+
+def build_scene(P, cfg):
+    n = cfg["n"]
+    pos, look = harness_camera(n)
+    planes = ()
+    if cfg.get("clip"):
+        planes = (P.clip_plane((n / 2.0,) * 3, (0.3, -0.5, 0.81)),)
+    return P.SceneState(camera=P.Camera(pos, look, image_size=cfg["image"]),
+                        tf_points={0: [(0.0, 0.0, 0.0, 0.0, 0.0), (1.0, 1.0, 1.0, 1.0, 1.0)]},
+                        value_ranges={0: (-0.4, 2.4)}, chain_texts={0: ""},
+                        settings=P.RenderSettings(active_set=(0,), interpolation=True, step_length=0.5,
+                                                  early_termination_alpha=1.0),
+                        clip_planes=planes)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"isc_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sms, maxs, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as fh:
+            for line in fh:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sms.append(float(parts[1]))
+                    maxs.append(float(parts[2]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        if not sms:
+            return None
+        return {"sm_mhz": statistics.median(sms), "sm_max_mhz": max(maxs), "reasons": sorted(reasons),
+                "samples": len(sms)}
+
+
+# --------------------------------------------------------------------------
+# B200 arm
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1611_09048_b200 as P
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = CONFIGS[args.config]
+    n = cfg["n"]
+    w, h = cfg["image"]
+    decomp = DECOMP[world]
+    volume = P.GlobalVolume((n, n, n), decomp)
+    domain = volume.local_domain(rank, 1)
+    t0 = time.time()
+    field = make_field_torch(n, domain, dev)
+    torch.cuda.synchronize()
+    log(f"[rank {rank}] field {tuple(field.shape)} ready in {time.time() - t0:.1f}s")
+    reg = P.SourceRegistry(domain)
+    reg.register_handle(P.array_backed_handle(P.SourceDescriptor("density", 1, has_guard=True), field, 1))
+    P.update_sources(reg, {0}, {})
+    fr = P.default_registry()
+    scene = build_scene(P, cfg)
+    order = P.visibility_order(volume, scene.camera)
+    if world > 1:
+        host = P.TorchDistTransport()
+        transport = P.NvlinkTransport(host, w * h)
+        canvas = transport.canvas(h, w)
+    else:
+        transport = P.LocalFabric(1).endpoint(0)
+        canvas = torch.empty((h, w, 4), dtype=torch.float32, device=dev)
+    ctx = P.RankContext(volume, domain, reg, fr, fr.limits, transport)
+    plans = P.build_plans(reg, fr, fr.limits, scene)
+    stream = torch.cuda.current_stream()
+
+    def step(events=None):
+        img = P.render_local(ctx, scene, plans=plans, out=canvas, check_errors=False, events=events)
+        full = P.binary_swap(transport, img.pixels, order)
+        return img, full
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up (also: station count of this brick, guard-contract check)
+    img = None
+    for _ in range(max(args.warmup, 1)):
+        img, _ = step()
+    img.check()
+    stations = img.stations
+    st_t = torch.tensor([stations], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(st_t)
+    samples_frame = int(st_t.item())
+
+    clocks = ClockSampler(local)
+    k = args.steps
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    start.record(stream)
+    for i in range(k):
+        step(evs[i])
+    end.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms_total = start.elapsed_time(end)
+    kernel_ms = sum(a.elapsed_time(b) for a, b in evs) / k
+    t = torch.tensor([ms_total, kernel_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total, kernel_ms_max = float(t[0]), float(t[1])
+    ms_step = ms_total / k
+    fps = 1000.0 / ms_step
+    gsps = samples_frame * fps / 1e9
+
+    # roofline of the dominant kernel (the march): algorithmic bytes per launch
+    bytes_rank = stations * BYTES_PER_SAMPLE + w * h * BYTES_PER_PIXEL_OUT
+    br = torch.tensor([float(bytes_rank)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(br)
+    peak, peak_src = peak_hbm()
+    achieved = float(br.item()) / (kernel_ms_max * 1e-3) / 1e9 / world
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            traffic = json.load(fh).get(f"{args.config}_n{world}")
+    except Exception:
+        pass
+
+    # e2e through the public API with host buffers: scene bytes in (JSON, as
+    # broadcast by the reference runtime) -> LUT + launch block H2D, frame out
+    # to pinned host memory (D2H) every step.
+    e2e = run_e2e(P, torch, dist, ctx, scene, transport, canvas, order, rank, world, dev, max(2, k // 2))
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(field, domain, volume, scene, samples_frame, budget_s=args.cpu_budget)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(fps, 3), "unit": "frames/s", "n_gpus": world, "steps": k,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"C4: {cfg['desc']}" if args.config == "c4" else cfg["desc"],
+                       "volume": [n, n, n], "image": [w, h], "decomposition": list(decomp),
+                       "samples_per_frame": samples_frame, "field_bytes_per_gpu": field.numel() * 4,
+                       "l2": "inputs larger than L2 (field >> 126 MB); no flush needed",
+                       "parallelism": f"bricks{decomp[0]}x{decomp[1]}x{decomp[2]}"},
+            "gsamples_per_s": round(gsps, 3),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "march_kernel<FAST,INTERP>", "kernel_ms": round(kernel_ms_max, 4),
+                         "algorithmic_bytes_per_launch": int(br.item() / world)},
+            "e2e": e2e,
+            "gpu_launches": k * (1 + (1 if world > 1 else 0)),
+            "clocks": clk,
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(P, torch, dist, ctx, scene, transport, canvas, order, rank, world, dev, steps):
+    from paper_1611_09048_b200.device import LUTS
+    w, h = scene.camera.image_size
+    payload = scene.to_bytes()
+    host_frame = torch.empty((h, w, 4), dtype=torch.float32).pin_memory() if rank == 0 else None
+    stream = torch.cuda.current_stream()
+    h2d = 0
+
+    def one():
+        nonlocal h2d
+        sc = P.SceneState.from_bytes(payload)          # scene as received from the root
+        LUTS._cache.clear()                             # force the LUT upload of this step
+        img = P.render_local(ctx, sc, out=canvas, check_errors=False)
+        full = P.binary_swap(transport, img.pixels, order)
+        if full is not None:
+            host_frame.copy_(full, non_blocking=True)
+        return full
+
+    one()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(steps):
+        one()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms_step = float(tt.item()) / steps
+    import ctypes
+    from paper_1611_09048_b200 import _abi
+    h2d = 256 * 4 * 4 + ctypes.sizeof(_abi.RenderArgs)
+    return {"value": round(1000.0 / ms_step, 3), "unit": "frames/s", "ms_per_step": round(ms_step, 4),
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": (w * h * 16) if rank == 0 else 0,
+            "path": "SceneState.from_bytes -> render_local -> binary_swap -> pinned host frame",
+            "note": "field is simulation-resident in HBM (in-situ zero-copy contract, fields.py:249-278); "
+                    "per-step host inputs are the scene (LUT + launch block), output the float32 frame"}
+
+
+# --------------------------------------------------------------------------
+# CPU baselines (oracle port; the reference itself is pure Python and cannot
+# travel to the GPU box -- DESIGN.md)
+
+
+def _frame_rays(n, image):
+    from oracle import isaac_oracle as O
+    pos, look = harness_camera(n)
+    w, h = image
+    return pos, O.primary_rays(pos, look, (0.0, 1.0, 0.0), math.radians(45.0), w, h)
+
+
+def _row_samples(n, image, pos, dirs, step=0.5):
+    """Stations per image row for the full volume (oracle ray setup only)."""
+    from oracle import isaac_oracle as O
+    w, h = image
+    o = O.np.asarray(pos)
+    ti, to = O.slab(o, dirs, O.np.zeros(3), O.np.full(3, float(n)))
+    hit = O.hit_mask(ti, to)
+    lo, hi = O.station_range(O.np.where(hit, ti, 0.0), O.np.where(hit, to, 0.0), step)
+    per_px = O.np.where(hit, hi - lo, 0)
+    return per_px.reshape(h, w).sum(axis=1)
+
+
+def _pick_rows(per_row, budget_samples):
+    import numpy as np
+    order = np.argsort(np.arange(len(per_row)) % 7, kind="stable")   # spread picks over the frame
+    rows, tot = [], 0
+    stride = max(1, int(per_row.sum() / max(budget_samples, 1)))
+    for r in range(0, len(per_row), stride):
+        rows.append(r)
+        tot += int(per_row[r])
+    del order
+    return rows, tot
+
+
+def _oracle_rows(args_tuple):
+    rows, = args_tuple
+    import numpy as np
+    from oracle import isaac_oracle as O
+    g = _WORKER
+    sel = np.concatenate([np.arange(r * g["w"], (r + 1) * g["w"]) for r in rows])
+    res = O.render_rays(g["pos"], g["dirs"][sel], g["brick"], [g["src"]], step=0.5, alpha_stop=1.0, interp=True)
+    return int(res.stations.sum())
+
+
+_WORKER: dict = {}
+
+
+def cpu_baseline(field_t, domain, volume, scene, samples_frame, budget_s=15.0, cores=1):
+    """Oracle (float64 numpy restatement of the reference path) on a bounded
+    sample of image rows of the same workload, timed on the host."""
+    import numpy as np
+    from oracle import isaac_oracle as O
+    n = volume.size[0]
+    image = scene.camera.image_size
+    arr = field_t.cpu().numpy() if hasattr(field_t, "cpu") else field_t
+    pos, dirs = _frame_rays(n, image)
+    per_row = _row_samples(n, image, pos, dirs)
+    rate_guess = 1.5e6 * cores
+    rows, expect = _pick_rows(per_row, int(rate_guess * budget_s))
+    src = O.Source(array=arr, offset=domain.offset, size=domain.size, guard=domain.guard_width,
+                   lut=O.lut_from_points([(0, 0, 0, 0, 0), (1, 1, 1, 1, 1)]), value_range=(-0.4, 2.4))
+    brick = O.Brick(domain.offset, domain.size, domain.guard_width, volume.size, volume.decomposition)
+    _WORKER.update(pos=pos, dirs=dirs, w=image[0], brick=brick, src=src)
+    t0 = time.perf_counter()
+    if cores == 1:
+        done = _oracle_rows((rows,))
+    else:
+        import multiprocessing as mp
+        chunks = [rows[i::cores * 4] for i in range(cores * 4) if rows[i::cores * 4]]
+        with mp.get_context("fork").Pool(cores) as pool:
+            done = sum(pool.map(_oracle_rows, [(c,) for c in chunks]))
+    dt = time.perf_counter() - t0
+    sps = done / dt
+    fps = sps / samples_frame
+    return {"value": round(fps, 6), "unit": "frames/s", "cores": cores, "kind": "port",
+            "samples_per_s": round(sps, 1),
+            "sample": f"{len(rows)} of {image[1]} image rows ({done} of {samples_frame} samples) of the same "
+                      f"{n}^3 x {image[0]}x{image[1]} frame, oracle/isaac_oracle.py render_rays, {dt:.1f}s"}
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm (oracle port, all host cores)."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import numpy as np
+
+    import paper_1611_09048_b200 as P
+    from oracle import isaac_oracle as O
+    cfg = CONFIGS[args.config]
+    n = cfg["n"]
+    w, h = cfg["image"]
+    decomp = DECOMP[world]
+    volume = P.GlobalVolume((n, n, n), (1, 1, 1))
+    domain = volume.local_domain(0, 1)
+    cores = os.cpu_count() or 1
+    # host field, same formula as the GPU arm (float32)
+    t0 = time.time()
+    import torch
+    torch.set_num_threads(cores)
+    field = make_field_torch(n, domain, "cpu").numpy()
+    log(f"[reference] host field ready in {time.time() - t0:.1f}s, {cores} cores")
+    scene = build_scene(P, cfg)
+    pos, dirs = _frame_rays(n, cfg["image"])
+    per_row = _row_samples(n, cfg["image"], pos, dirs)
+    samples_frame = int(per_row.sum())
+    src = O.Source(array=field, offset=domain.offset, size=domain.size, guard=1,
+                   lut=O.lut_from_points([(0, 0, 0, 0, 0), (1, 1, 1, 1, 1)]), value_range=(-0.4, 2.4))
+    brick = O.Brick(domain.offset, domain.size, 1, volume.size, volume.decomposition)
+    _WORKER.update(pos=pos, dirs=dirs, w=w, brick=brick, src=src)
+    rows, _ = _pick_rows(per_row, int(1.2e6 * cores * args.ref_step_s))
+    import multiprocessing as mp
+    chunks = [rows[i::cores] for i in range(cores) if rows[i::cores]]
+    with mp.get_context("fork").Pool(cores) as pool:
+        for _ in range(args.warmup):
+            pool.map(_oracle_rows, [(c,) for c in chunks])
+        t0 = time.perf_counter()
+        done = 0
+        for _ in range(args.steps):
+            done += sum(pool.map(_oracle_rows, [(c,) for c in chunks]))
+        dt = time.perf_counter() - t0
+    sps = done / dt
+    fps = sps / samples_frame
+    line = {"metric": METRIC, "value": round(fps, 6), "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(1000.0 / fps, 1), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"C4: {cfg['desc']}", "volume": [n, n, n], "image": [w, h],
+                       "decomposition": list(decomp), "samples_per_frame": samples_frame},
+            "gsamples_per_s": round(sps / 1e9, 6),
+            "cpu_baseline": {"value": round(fps, 6), "unit": "frames/s", "cores": cores, "kind": "port",
+                             "sample": f"per step {len(rows)} of {h} image rows of the {n}^3 frame "
+                                       f"({done // max(args.steps, 1)} samples), oracle/isaac_oracle.py "
+                                       f"render_rays over {cores} worker processes"},
+            "e2e": {"value": round(fps, 6), "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--ref-step-s", type=float, default=4.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("note: warmup < 3 requested; using 3")
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

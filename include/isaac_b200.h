@@ -1,0 +1,232 @@
+/*
+ * isaac_b200.h -- C-ABI of the B200 (sm_100a) ISAAC rendering hot path.
+ *
+ * One shared library (libisaac_b200.so) exporting plain extern "C" entry
+ * points: POD structs, raw device pointers, element counts and a CUDA stream
+ * passed as void*.  No torch types cross this boundary; the Python host layer
+ * (paper_1611_09048_b200/) binds it with ctypes, exactly as the reference's
+ * Python API would (see INTEGRATION.md for the binding stub).
+ *
+ * Every call is stream-ordered and asynchronous unless stated otherwise.
+ * Return value: ISC_OK or an isc_status; isc_last_error() gives the
+ * thread-local message.  Status codes map 1:1 onto the reference exceptions:
+ *   ISC_E_FIELD    -> fields.FieldError          (fields.py:24-25)
+ *   ISC_E_GUARD    -> fields.GuardContractError  (fields.py:32-33)
+ *   ISC_E_CHAIN    -> functors.ChainError        (functors.py:20-21)
+ *   ISC_E_SCENE    -> scene.SceneError           (scene.py:21-22)
+ *   ISC_E_COMPOSITE-> compositing.CompositeError (compositing.py:21-22)
+ *   ISC_E_TRANSPORT-> transport.TransportError   (transport.py:16-17)
+ *   ISC_E_VALUE    -> ValueError                 (raycast.py:76-77, 156-157)
+ *
+ * Reference interfaces replaced (all under /root/reference/pkg/src/insitu/):
+ *   isc_render_local   <- raycast.render_local       raycast.py:492-541
+ *                         (+ march_rays 291-381, _iso_detect 384-468,
+ *                            gradient_normals 210-242, _trilinear 182-199,
+ *                            fields.sample_many 218-246, eval_chain_array
+ *                            functors.py:212-222, classify_array scene.py:139-152)
+ *   isc_ray_setup      <- Camera.ray_directions scene.py:55-70,
+ *                         _ray_box_intervals raycast.py:100-120,
+ *                         _apply_clip_planes raycast.py:123-143,
+ *                         hit mask raycast.py:522, station range raycast.py:316-324
+ *   isc_value_range    <- (no reference function; value ranges are scene
+ *                         state, scene.py:188 / runtime.py:154-157)
+ *   isc_over           <- compositing.over_arrays   compositing.py:31-33
+ *   isc_composite_fold <- compositing.composite_sequential compositing.py:66-77
+ *                         and _direct_send           compositing.py:184-194
+ *   isc_binary_swap    <- compositing.binary_swap   compositing.py:107-181
+ *   isc_arena_* / isc_ipc_* <- transport.Transport  transport.py:20-28
+ *                         (the NVLink replacement of LocalFabric queues)
+ */
+#ifndef ISAAC_B200_H
+#define ISAAC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define ISC_API __attribute__((visibility("default")))
+#else
+#define ISC_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ISC_ABI_VERSION 1
+#define ISC_MAX_SOURCES 8      /* active sources per render                 */
+#define ISC_MAX_CLIP_PLANES 8
+#define ISC_MAX_CHAIN 8        /* ChainLimits.max_length default is 5        */
+#define ISC_LUT_ENTRIES 256    /* scene.py:18                                 */
+#define ISC_MAX_RANKS 64
+#define ISC_MAX_ROUNDS 6       /* log2(ISC_MAX_RANKS)                         */
+#define ISC_IPC_HANDLE_BYTES 64
+
+typedef enum {
+  ISC_OK = 0,
+  ISC_E_FIELD = 1,
+  ISC_E_GUARD = 2,
+  ISC_E_CHAIN = 3,
+  ISC_E_SCENE = 4,
+  ISC_E_COMPOSITE = 5,
+  ISC_E_TRANSPORT = 6,
+  ISC_E_VALUE = 7,
+  ISC_E_CUDA = 8
+} isc_status;
+
+typedef enum { ISC_F32 = 0, ISC_F64 = 1, ISC_F16 = 2, ISC_BF16 = 3 } isc_dtype;
+typedef enum { ISC_VOLUME = 0, ISC_ISO = 1 } isc_mode;
+
+/* Functor-chain opcodes.  1..5 are the reference built-ins
+ * (functors.py:124-147); the rest are device ops for user-registered
+ * functors (FunctorRegistry.register_functor, functors.py:81-90). */
+typedef enum {
+  ISC_OP_ADD = 1, ISC_OP_MUL = 2, ISC_OP_POW = 3, ISC_OP_LENGTH = 4, ISC_OP_SUM = 5,
+  ISC_OP_SQRT = 6, ISC_OP_ABS = 7, ISC_OP_NEG = 8, ISC_OP_EXP = 9, ISC_OP_LOG = 10,
+  ISC_OP_MIN = 11, ISC_OP_MAX = 12
+} isc_op;
+
+typedef struct {
+  int32_t op;        /* isc_op                                    */
+  int32_t in_dim;    /* dimension entering this step (1..4)       */
+  float arg[4];      /* constant, already broadcast (functors.py:191-194) */
+} isc_chain_step;
+
+/* One active source: a zero-copy view of an application array laid out
+ * (z, y, x[, component]) INCLUDING the guard halo, as array_backed_handle
+ * expects (fields.py:249-278). */
+typedef struct {
+  const void* data;          /* device pointer to element [0,0,0,0]      */
+  int64_t stride[4];         /* element strides of z, y, x, component     */
+  int32_t dtype;             /* isc_dtype                                 */
+  int32_t feature_dim;       /* 1..4                                      */
+  int32_t has_guard;         /* SourceDescriptor.has_guard                */
+  int32_t mode;              /* isc_mode                                  */
+  float iso_threshold;
+  float range_lo, range_hi;  /* TransferFunction.value_range              */
+  int32_t n_steps;           /* chain length (0 = identity)               */
+  const float* lut;          /* device, 256 x 4 straight RGBA (float32)  */
+  isc_chain_step steps[ISC_MAX_CHAIN];
+} isc_source;
+
+/* Camera in global cell coordinates; basis/tan/aspect precomputed on the
+ * host with the reference's numpy expressions (scene.py:46-62). */
+typedef struct {
+  double origin[3];
+  double fwd[3], right[3], up[3];
+  double tan_half, aspect;
+  int32_t width, height;
+} isc_camera;
+
+/* Clip plane (scene.py:73-93); f0 = np.dot(origin - point, normal)
+ * evaluated on the host exactly as raycast.py:133 does. */
+typedef struct {
+  double point[3];
+  double normal[3];
+  double f0;
+} isc_clip_plane;
+
+typedef struct {
+  isc_camera camera;
+  double step;               /* RenderSettings.step_length                */
+  double alpha_stop;         /* early_termination_alpha; >= 1 disables    */
+  int32_t interpolation;     /* 1 = trilinear, 0 = nearest                */
+  int32_t n_sources;         /* active sources in source-id order         */
+  int32_t n_clip;
+  int32_t guard_width;       /* LocalDomain.guard_width                   */
+  int32_t brick_offset[3];   /* LocalDomain.offset (x, y, z)             */
+  int32_t brick_size[3];     /* LocalDomain.size                          */
+  int32_t volume_size[3];    /* GlobalVolume.size                         */
+  int32_t decomposition[3];  /* GlobalVolume.decomposition                */
+  isc_clip_plane clip[ISC_MAX_CLIP_PLANES];
+  isc_source src[ISC_MAX_SOURCES];
+  /* outputs (device pointers, caller-owned) */
+  float* out_rgba;           /* (H, W, 4) premultiplied; required         */
+  uint32_t* out_stations;    /* (H*W) stations marched per pixel; optional */
+  int32_t* out_krange;       /* (H*W, 4) k_lo, k_hi, kg_lo, kg_hi; optional */
+  double* out_t;             /* (H*W, 2) t_in, t_out of the brick; optional */
+  uint8_t* out_hit;          /* (H*W) hit mask; optional                  */
+  uint32_t* error_word;      /* device u32; guard-contract violations are
+                                counted here (-> GuardContractError); optional */
+  unsigned long long* out_station_total; /* device u64: sum of stations marched
+                                (LocalImage.stations, raycast.py:46); optional */
+} isc_render_args;
+/* isc_render_local zeroes *error_word and *out_station_total (stream-ordered)
+ * before the march, so callers never need a separate fill. */
+
+/* ---- library ------------------------------------------------------------ */
+ISC_API int isc_abi_version(void);
+ISC_API const char* isc_last_error(void);
+/* sizeof of the public structs, so bindings can verify their layouts:
+ * which = 0 isc_render_args, 1 isc_source, 2 isc_camera, 3 isc_clip_plane,
+ * 4 isc_chain_step, 5 isc_swap_args */
+ISC_API size_t isc_struct_size(int which);
+ISC_API int isc_device_sm_count(int device);
+
+/* ---- rendering ---------------------------------------------------------- */
+/* Full brick render (ray setup + march + iso + compositing in registers). */
+ISC_API int isc_render_local(const isc_render_args* args, void* stream);
+/* Ray setup only (parity/debug): fills out_t / out_krange / out_hit. */
+ISC_API int isc_ray_setup(const isc_render_args* args, void* stream);
+/* Per-source normalisation: (min, max) of the float32-chained first
+ * component over the brick interior (guard excluded), NaN ignored.
+ * out_minmax: device buffer of >= 4 32-bit words; [0], [1] receive (min, max)
+ * as float32 (NaN, NaN if no non-NaN value), [2], [3] are scratch.
+ * Bit-exact for add/mul/length/sum chains. */
+ISC_API int isc_value_range(const isc_source* src, const int32_t brick_size[3], int32_t guard_width,
+                    float* out_minmax, void* stream);
+
+/* ---- compositing ---------------------------------------------------------- */
+/* dst[i] = front[i] over back[i] (premultiplied RGBA float32). */
+ISC_API int isc_over(float* dst, const float* front, const float* back, int64_t n_pixels, void* stream);
+/* out = images[0] over images[1] over ... (front to back, float32 RGBA);
+ * images is a HOST array of device (or peer-mapped) pointers. */
+ISC_API int isc_composite_fold(float* out, const float* const* images, int32_t n_images,
+                       int64_t n_pixels, void* stream);
+
+/* Binary swap over peer memory.  Every rank runs one persistent kernel; in
+ * round r it pulls its partner's half-span straight out of the partner's
+ * image (NVLink peer load), composites it with its own half in visibility
+ * order and writes it in place; after the last round every rank stores its
+ * 1/R span directly into rank 0's output.  Cross-GPU ordering uses
+ * epoch-tagged arrival counters in each rank's flag block (no host round
+ * trips).  Pointers for other ranks are peer-mapped (isc_ipc_open) or, for
+ * ranks sharing one device, plain device pointers. */
+typedef struct {
+  int32_t rank, size;            /* this rank, world size (power of two) */
+  int32_t n_ctas;                /* fixed grid of the exchange kernel    */
+  int32_t round_begin, round_end;/* rounds executed by this launch       */
+  int32_t collect;               /* 1: store final span into root_out    */
+  int32_t finish;                /* 1: wait until peers stopped reading  */
+  int32_t publish_ready;         /* 1: announce this rank's image ready  */
+  int64_t n_pixels;
+  int64_t epoch;                 /* 1, 2, 3, ... identical on all ranks  */
+  int64_t timeout_ns;            /* spin-wait limit -> ISC_E_TRANSPORT   */
+  int32_t order[ISC_MAX_RANKS];  /* visibility order (compositing.py:36-63) */
+  float* image[ISC_MAX_RANKS];   /* every rank's working image           */
+  unsigned long long* flags[ISC_MAX_RANKS]; /* every rank's flag block   */
+  float* root_out;               /* rank 0's output image                */
+} isc_swap_args;
+ISC_API int isc_binary_swap(const isc_swap_args* args, void* stream);
+/* Number of 8-byte words in a rank's flag block. */
+ISC_API int isc_flag_words(void);
+/* Read-and-clear this rank's transport error word (device -> host, syncs). */
+ISC_API int isc_swap_status(unsigned long long* flags, void* stream, int32_t* out_code);
+
+/* Direct-send fallback for non-power-of-two world sizes: rank 0 folds every
+ * rank's image (peer loads) in visibility order into root_out; other ranks
+ * publish readiness and wait until rank 0 has finished reading them. */
+ISC_API int isc_direct_send(const isc_swap_args* args, void* stream);
+
+/* ---- device memory shared between processes --------------------------- */
+ISC_API int isc_arena_alloc(size_t bytes, void** out_ptr);     /* cudaMalloc + zero */
+ISC_API int isc_arena_free(void* ptr);
+ISC_API int isc_ipc_handle(void* dev_ptr, unsigned char out_handle[ISC_IPC_HANDLE_BYTES]);
+ISC_API int isc_ipc_open(const unsigned char handle[ISC_IPC_HANDLE_BYTES], void** out_ptr);
+ISC_API int isc_ipc_close(void* peer_ptr);
+ISC_API int isc_enable_peer_access(int peer_device);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ISAAC_B200_H */

@@ -381,17 +381,27 @@ def render_brick(camera: dict, brick: Brick, sources: Sequence[Source], *, step=
     ``sources``: the active sources in source-id order.
     """
     w, h = camera["width"], camera["height"]
-    origin = np.asarray(camera["position"], dtype=np.float64)
     if dirs is None:
         dirs = primary_rays(camera["position"], camera["look_at"], camera.get("up", (0.0, 1.0, 0.0)),
                             camera.get("vertical_fov", math.radians(45.0)), w, h)
+    res = render_rays(camera["position"], dirs, brick, sources, step=step, alpha_stop=alpha_stop,
+                      interp=interp, planes=planes, recorder=recorder)
+    res.rgba = res.rgba.reshape(h, w, 4)
+    return res
+
+
+def render_rays(position, dirs, brick: Brick, sources: Sequence[Source], *, step=0.5, alpha_stop=1.0,
+                interp=True, planes=(), recorder: Optional[Callable] = None) -> RenderResult:
+    """The per-ray body of :func:`render_brick` for an arbitrary ray list
+    (``rgba`` comes back flat, (n, 4))."""
+    origin = np.asarray(position, dtype=np.float64)
     lo = np.asarray(brick.offset, dtype=np.float64)
     hi = lo + np.asarray(brick.size, dtype=np.float64)
     t_in, t_out = clip(origin, dirs, *slab(origin, dirs, lo, hi), planes)
     g_in, g_out = clip(origin, dirs, *slab(origin, dirs, np.zeros(3),
                                             np.asarray(brick.volume_size, dtype=np.float64)), planes)
     hit = hit_mask(t_in, t_out)
-    npx = w * h
+    npx = dirs.shape[0]
     k_lo = np.zeros(npx, np.int64)
     k_hi = np.zeros(npx, np.int64)
     kg_lo = np.zeros(npx, np.int64)
@@ -407,7 +417,7 @@ def render_brick(camera: dict, brick: Brick, sources: Sequence[Source], *, step=
                            None if recorder is None else (lambda k, sub: recorder(k, rays[sub])))
         image[rays] = rgba
         per_px[rays] = cnt
-    return RenderResult(image.reshape(h, w, 4), per_px, hit, t_in, t_out, k_lo, k_hi, kg_lo, kg_hi)
+    return RenderResult(image, per_px, hit, t_in, t_out, k_lo, k_hi, kg_lo, kg_hi)
 
 
 def _march(origin, dirs, k_lo, k_hi, kg_lo, kg_hi, brick, sources, step, alpha_stop, interp, recorder):

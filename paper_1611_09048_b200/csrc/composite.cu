@@ -1,0 +1,322 @@
+// K5-K7: sort-last compositing over peer memory.
+//
+//   isc_over            over_arrays           compositing.py:31-33
+//   isc_composite_fold  composite_sequential  compositing.py:66-77
+//   isc_binary_swap     binary_swap           compositing.py:107-181
+//   isc_direct_send     _direct_send          compositing.py:184-194
+//
+// The swap is ONE persistent kernel per rank: every round pulls the
+// partner's half-span straight out of the partner's image through its
+// peer-mapped pointer (NVLink 5 loads on a multi-GPU box), composites it with
+// the local half in visibility order and writes the result in place, so the
+// transfer and the `over` are the same instruction stream.  After the last
+// round each rank stores its 1/R span directly into rank 0's output (the
+// collection step of compositing.py:169-181).  Ranks order themselves through
+// epoch-tagged arrival counters living in each rank's flag block: a CTA
+// publishes "stage s done" with a system-scope release add, a reader spins on
+// a system-scope acquire load of its peer's counter (bounded by a timeout so a
+// missing peer surfaces as TransportError instead of a hung GPU).
+#include <cstring>
+
+#include "common.cuh"
+
+namespace isc {
+
+constexpr int kFlagWords = 16;
+constexpr int kErrWord = 9;
+constexpr int kRootReadWord = 8;
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Thread 0 spins until *p >= target; returns false on timeout (and records
+// the error in the local flag block).  Caller must __syncthreads afterwards.
+__device__ bool wait_at_least(const unsigned long long* p, unsigned long long target, long long timeout_ns,
+                              unsigned long long* my_flags) {
+  const unsigned long long t0 = global_ns();
+  unsigned int backoff = 32;
+  while (ld_acquire_sys(p) < target) {
+    if ((long long)(global_ns() - t0) > timeout_ns) {
+      atomicExch(my_flags + kErrWord, 1ull);
+      return false;
+    }
+    __nanosleep(backoff);
+    if (backoff < 1024) backoff <<= 1;
+  }
+  return true;
+}
+
+__device__ __forceinline__ void publish(unsigned long long* flags, int word) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    red_release_sys(flags + word, 1ull);
+  }
+}
+
+// Returns false if any thread of the CTA saw a timeout.
+__device__ __forceinline__ bool cta_wait(const unsigned long long* p, unsigned long long target, long long tmo,
+                                         unsigned long long* my_flags) {
+  __shared__ int ok;
+  if (threadIdx.x == 0) ok = wait_at_least(p, target, tmo, my_flags) ? 1 : 0;
+  __syncthreads();
+  const bool r = ok != 0;
+  __syncthreads();
+  return r;
+}
+
+__global__ void over_kernel(float4* dst, const float4* front, const float4* back, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    dst[i] = over4(__ldcg(front + i), __ldcg(back + i));
+}
+
+struct FoldArgs {
+  const float4* img[ISC_MAX_RANKS];
+  int n;
+};
+
+__global__ void fold_kernel(float4* out, const __grid_constant__ FoldArgs f, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int r = 0; r < f.n; ++r) acc = over4(acc, __ldcg(f.img[r] + i));
+    out[i] = acc;
+  }
+}
+
+__device__ __forceinline__ void cta_chunk(long long lo, long long hi, long long& a, long long& b) {
+  const long long n = hi - lo;
+  const long long per = (n + gridDim.x - 1) / gridDim.x;
+  a = lo + per * blockIdx.x;
+  b = min(hi, a + per);
+  if (a > hi) a = hi;
+}
+
+__global__ void __launch_bounds__(512) swap_kernel(const __grid_constant__ isc_swap_args a) {
+  const int R = a.size;
+  int v = 0;
+  for (int i = 0; i < R; ++i)
+    if (a.order[i] == a.rank) v = i;
+  int rounds = 0;
+  while ((1 << rounds) < R) ++rounds;
+  unsigned long long* me = a.flags[a.rank];
+  const unsigned long long target = (unsigned long long)a.epoch * (unsigned long long)a.n_ctas;
+  float4* mine = reinterpret_cast<float4*>(a.image[a.rank]);
+
+  if (a.publish_ready) publish(me, 0);  // image ready (stream-ordered after render)
+
+  long long lo = 0, hi = a.n_pixels;
+  for (int r = 0; r < rounds; ++r) {
+    const int bit = 1 << r;
+    const int pv = v ^ bit;
+    const long long mid = (lo + hi) / 2;
+    const bool keep_high = (v & bit) != 0;
+    const long long klo = keep_high ? mid : lo, khi = keep_high ? hi : mid;
+    if (r >= a.round_begin && r < a.round_end) {
+      const int partner = a.order[pv];
+      if (!cta_wait(a.flags[partner] + r, target, a.timeout_ns, me)) return;
+      if (r > 0 && !cta_wait(me + r, target, a.timeout_ns, me)) return;
+      const float4* theirs = reinterpret_cast<const float4*>(a.image[partner]);
+      long long c0, c1;
+      cta_chunk(klo, khi, c0, c1);
+      const bool partner_front = pv < v;
+      for (long long i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+        const float4 m = __ldcg(mine + i), t = __ldcg(theirs + i);
+        mine[i] = partner_front ? over4(t, m) : over4(m, t);
+      }
+      publish(me, r + 1);
+    }
+    lo = klo;
+    hi = khi;
+  }
+
+  if (a.collect) {
+    if (!cta_wait(me + rounds, target, a.timeout_ns, me)) return;
+    float4* out = reinterpret_cast<float4*>(a.root_out);
+    long long c0, c1;
+    cta_chunk(lo, hi, c0, c1);
+    for (long long i = c0 + threadIdx.x; i < c1; i += blockDim.x) out[i] = __ldcg(mine + i);
+    publish(me, rounds + 1);
+  }
+
+  if (a.finish && blockIdx.x == 0) {
+    if (a.rank == 0) {
+      for (int q = 0; q < R; ++q)
+        if (!cta_wait(a.flags[q] + rounds + 1, target, a.timeout_ns, me)) return;
+    } else {
+      int vv = v;
+      for (int r = 0; r < rounds; ++r) {
+        const int partner = a.order[vv ^ (1 << r)];
+        if (!cta_wait(a.flags[partner] + r + 1, target, a.timeout_ns, me)) return;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(512) direct_send_kernel(const __grid_constant__ isc_swap_args a) {
+  unsigned long long* me = a.flags[a.rank];
+  const unsigned long long target = (unsigned long long)a.epoch * (unsigned long long)a.n_ctas;
+  if (a.publish_ready) publish(me, 0);
+  if (a.rank == 0) {
+    for (int q = 0; q < a.size; ++q)
+      if (!cta_wait(a.flags[q], target, a.timeout_ns, me)) return;
+    long long c0, c1;
+    cta_chunk(0, a.n_pixels, c0, c1);
+    float4* out = reinterpret_cast<float4*>(a.root_out);
+    for (long long i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int r = 0; r < a.size; ++r)
+        acc = over4(acc, __ldcg(reinterpret_cast<const float4*>(a.image[a.order[r]]) + i));
+      out[i] = acc;
+    }
+    publish(me, kRootReadWord);
+  } else if (a.finish && blockIdx.x == 0) {
+    cta_wait(a.flags[0] + kRootReadWord, target, a.timeout_ns, me);
+  }
+}
+
+static int grid_for(long long n) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  long long g = (n + 255) / 256;
+  const long long cap = (long long)sms * 8;
+  return (int)(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+static int check_swap(const isc_swap_args* a, bool pow2) {
+  if (!a) return fail(ISC_E_VALUE, "null swap args");
+  if (a->size < 1 || a->size > ISC_MAX_RANKS) return fail(ISC_E_COMPOSITE, "world size out of range");
+  if (a->rank < 0 || a->rank >= a->size) return fail(ISC_E_COMPOSITE, "rank out of range");
+  if (pow2 && (a->size & (a->size - 1))) return fail(ISC_E_COMPOSITE, "binary swap needs a power-of-two size");
+  if (a->n_ctas < 1 || a->n_ctas > 4096) return fail(ISC_E_COMPOSITE, "n_ctas out of range");
+  if (a->epoch < 1) return fail(ISC_E_COMPOSITE, "epoch must start at 1");
+  unsigned seen = 0;
+  unsigned long long seen_hi = 0;
+  for (int i = 0; i < a->size; ++i) {
+    const int o = a->order[i];
+    if (o < 0 || o >= a->size) return fail(ISC_E_COMPOSITE, "order entry out of range");
+    if (o < 32) { if (seen & (1u << o)) return fail(ISC_E_COMPOSITE, "order is not a permutation"); seen |= 1u << o; }
+    else { if (seen_hi & (1ull << (o - 32))) return fail(ISC_E_COMPOSITE, "order is not a permutation"); seen_hi |= 1ull << (o - 32); }
+    if (!a->image[i] || !a->flags[i]) return fail(ISC_E_COMPOSITE, "missing image/flag pointer");
+  }
+  return ISC_OK;
+}
+
+}  // namespace isc
+
+using namespace isc;
+
+extern "C" int isc_over(float* dst, const float* front, const float* back, int64_t n, void* stream) {
+  if (n < 0 || (n > 0 && (!dst || !front || !back))) return fail(ISC_E_VALUE, "bad over arguments");
+  if (n == 0) return ISC_OK;
+  over_kernel<<<grid_for(n), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<float4*>(dst), reinterpret_cast<const float4*>(front), reinterpret_cast<const float4*>(back), n);
+  ISC_CUDA_CHECK(cudaGetLastError());
+  return ISC_OK;
+}
+
+extern "C" int isc_composite_fold(float* out, const float* const* images, int32_t n_images, int64_t n, void* stream) {
+  if (!out || !images || n_images < 1 || n_images > ISC_MAX_RANKS || n < 0)
+    return fail(ISC_E_COMPOSITE, "bad fold arguments");
+  if (n == 0) return ISC_OK;
+  FoldArgs f;
+  f.n = n_images;
+  for (int i = 0; i < n_images; ++i) {
+    if (!images[i]) return fail(ISC_E_COMPOSITE, "null image pointer");
+    f.img[i] = reinterpret_cast<const float4*>(images[i]);
+  }
+  fold_kernel<<<grid_for(n), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(reinterpret_cast<float4*>(out), f, n);
+  ISC_CUDA_CHECK(cudaGetLastError());
+  return ISC_OK;
+}
+
+extern "C" int isc_binary_swap(const isc_swap_args* a, void* stream) {
+  int st = check_swap(a, true);
+  if (st != ISC_OK) return st;
+  if (a->collect && !a->root_out) return fail(ISC_E_COMPOSITE, "collect needs root_out");
+  swap_kernel<<<a->n_ctas, 512, 0, reinterpret_cast<cudaStream_t>(stream)>>>(*a);
+  ISC_CUDA_CHECK(cudaGetLastError());
+  return ISC_OK;
+}
+
+extern "C" int isc_direct_send(const isc_swap_args* a, void* stream) {
+  int st = check_swap(a, false);
+  if (st != ISC_OK) return st;
+  if (a->rank == 0 && !a->root_out) return fail(ISC_E_COMPOSITE, "root needs root_out");
+  direct_send_kernel<<<a->n_ctas, 512, 0, reinterpret_cast<cudaStream_t>(stream)>>>(*a);
+  ISC_CUDA_CHECK(cudaGetLastError());
+  return ISC_OK;
+}
+
+extern "C" int isc_flag_words(void) { return kFlagWords; }
+
+extern "C" int isc_swap_status(unsigned long long* flags, void* stream, int32_t* out_code) {
+  if (!flags || !out_code) return fail(ISC_E_VALUE, "null argument");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  unsigned long long v = 0;
+  ISC_CUDA_CHECK(cudaMemcpyAsync(&v, flags + kErrWord, sizeof(v), cudaMemcpyDeviceToHost, s));
+  ISC_CUDA_CHECK(cudaStreamSynchronize(s));
+  *out_code = (int32_t)v;
+  if (v) {
+    const unsigned long long zero = 0;
+    ISC_CUDA_CHECK(cudaMemcpyAsync(flags + kErrWord, &zero, sizeof(zero), cudaMemcpyHostToDevice, s));
+    ISC_CUDA_CHECK(cudaStreamSynchronize(s));
+  }
+  return ISC_OK;
+}
+
+extern "C" int isc_arena_alloc(size_t bytes, void** out_ptr) {
+  if (!out_ptr || bytes == 0) return fail(ISC_E_VALUE, "bad arena request");
+  ISC_CUDA_CHECK(cudaMalloc(out_ptr, bytes));
+  ISC_CUDA_CHECK(cudaMemset(*out_ptr, 0, bytes));
+  ISC_CUDA_CHECK(cudaDeviceSynchronize());
+  return ISC_OK;
+}
+
+extern "C" int isc_arena_free(void* ptr) {
+  if (ptr) ISC_CUDA_CHECK(cudaFree(ptr));
+  return ISC_OK;
+}
+
+extern "C" int isc_ipc_handle(void* dev_ptr, unsigned char out[ISC_IPC_HANDLE_BYTES]) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == ISC_IPC_HANDLE_BYTES, "ipc handle size");
+  if (!dev_ptr || !out) return fail(ISC_E_VALUE, "null argument");
+  cudaIpcMemHandle_t h;
+  ISC_CUDA_CHECK(cudaIpcGetMemHandle(&h, dev_ptr));
+  memcpy(out, &h, sizeof(h));
+  return ISC_OK;
+}
+
+extern "C" int isc_ipc_open(const unsigned char handle[ISC_IPC_HANDLE_BYTES], void** out_ptr) {
+  if (!handle || !out_ptr) return fail(ISC_E_VALUE, "null argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  ISC_CUDA_CHECK(cudaIpcOpenMemHandle(out_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return ISC_OK;
+}
+
+extern "C" int isc_ipc_close(void* p) {
+  if (p) ISC_CUDA_CHECK(cudaIpcCloseMemHandle(p));
+  return ISC_OK;
+}
+
+extern "C" int isc_enable_peer_access(int peer) {
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return ISC_OK;
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+  return ISC_OK;
+}

@@ -1,0 +1,305 @@
+// K1-K3: ray setup + front-to-back march + iso-surface detection for one
+// brick.  Replaces raycast.render_local (raycast.py:492-541) together with
+// march_rays (291-381), _iso_detect (384-468) and gradient_normals (210-242).
+//
+// Execution model: one thread per pixel, 16x16 pixel tile per CTA, each warp
+// an 8x4 sub-tile so the 32 rays of a warp stay spatially coherent and their
+// trilinear gathers share L1 lines.  Positions, cell indices and fractions
+// are float64 (bit-identical cell selection to the reference); field values,
+// chains, classification and the over-accumulation are float32.  The
+// transfer-function LUTs of all active sources live in shared memory.
+#include <math_constants.h>
+
+#include "common.cuh"
+#include "raysetup.cuh"
+#include "sample.cuh"
+
+namespace isc {
+
+constexpr int kTile = 16;
+constexpr int kThreads = kTile * kTile;
+
+__device__ __forceinline__ void tile_pixel(int& px, int& py) {
+  const int t = threadIdx.x, w = t >> 5, l = t & 31;
+  px = blockIdx.x * kTile + (w & 1) * 8 + (l & 7);
+  py = blockIdx.y * kTile + (w >> 1) * 4 + (l >> 3);
+}
+
+__device__ __forceinline__ Brick make_brick(const isc_render_args& a) {
+  Brick b;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    b.size[i] = a.brick_size[i];
+    b.offset[i] = (double)a.brick_offset[i];
+  }
+  b.guard = a.guard_width;
+  return b;
+}
+
+template <bool F32>
+__device__ __forceinline__ float scalar_at(const isc_source& s, const Brick& b, const double p[3], bool interp,
+                                           uint32_t* err) {
+  double l[3] = {dsub(p[0], b.offset[0]), dsub(p[1], b.offset[1]), dsub(p[2], b.offset[2])};
+  float v[4] = {0.f, 0.f, 0.f, 0.f};
+  sample_local<F32, 0>(s, b, l, interp, v, err);
+  return run_chain(s, v, s.feature_dim);
+}
+
+// raycast.py:270-278: trilinear gathers at p stay within the guard halo.
+__device__ __forceinline__ bool reachable(const double off[3], const double size[3], int g, const double p[3]) {
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const double lo = dsub(off[i], (double)g);
+    const double hi = dsub(dadd(dadd(off[i], size[i]), (double)g), 1.0);
+    ok &= (p[i] >= lo) && (p[i] < hi);
+  }
+  return ok;
+}
+
+// Central-difference normal of the chained scalar (raycast.py:210-242).
+__device__ float3 iso_normal(const isc_source& s, const Brick& b, const double p[3], const double d[3],
+                             bool interp, uint32_t* err) {
+  const int g = (s.has_guard && interp) ? b.guard : 0;
+  float grad[3];
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    const double lo = dsub(b.offset[ax], (double)g);
+    const double hi = dsub(dsub(dadd(dadd(lo, (double)b.size[ax]), (double)(2 * g)), 1.0), 1e-9);
+    double pp[3] = {p[0], p[1], p[2]}, pm[3] = {p[0], p[1], p[2]};
+    pp[ax] = dmin(dmax(dadd(p[ax], 1.0), lo), hi);
+    pm[ax] = dmin(dmax(dsub(p[ax], 1.0), lo), hi);
+    double span = dsub(pp[ax], pm[ax]);
+    if (span == 0.0) span = 1.0;
+    const float sp = scalar_at<false>(s, b, pp, interp, err);
+    const float sm = scalar_at<false>(s, b, pm, interp, err);
+    grad[ax] = (float)((double)(sp - sm) / span);
+  }
+  const float mag = sqrtf((grad[0] * grad[0] + grad[1] * grad[1]) + grad[2] * grad[2]);
+  if (mag < 1e-12f) {
+    const double dm = sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
+    return make_float3((float)(-d[0] / dm), (float)(-d[1] / dm), (float)(-d[2] / dm));
+  }
+  return make_float3(grad[0] / mag, grad[1] / mag, grad[2] / mag);
+}
+
+// FAST: exactly one active float32 scalar source in volume mode.
+template <bool FAST, bool INTERP>
+__global__ void __launch_bounds__(kThreads) march_kernel(const __grid_constant__ isc_render_args a) {
+  extern __shared__ float4 lut_s[];
+  for (int i = threadIdx.x; i < a.n_sources * ISC_LUT_ENTRIES; i += blockDim.x)
+    lut_s[i] = reinterpret_cast<const float4*>(a.src[i >> 8].lut)[i & (ISC_LUT_ENTRIES - 1)];
+  __syncthreads();
+
+  int px, py;
+  tile_pixel(px, py);
+  if (px >= a.camera.width || py >= a.camera.height) return;
+  const long long pix = (long long)py * a.camera.width + px;
+
+  Ray r;
+  setup_ray(a, px, py, r);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  uint32_t stations = 0;
+
+  if (r.hit) {
+    const Brick b = make_brick(a);
+    const double* o = a.camera.origin;
+    const bool gate_alpha = a.alpha_stop < 1.0;
+    uint32_t* err = a.error_word;
+
+    if constexpr (FAST) {
+      const isc_source& s = a.src[0];
+      const float lo = s.range_lo, inv = 1.0f / (s.range_hi - s.range_lo);
+      for (long long k = r.k_lo; k < r.k_hi; ++k) {
+        ++stations;
+        double p[3];
+        station_pos(o, r.d, dmul((double)k, a.step), p);
+        const double l[3] = {dsub(p[0], b.offset[0]), dsub(p[1], b.offset[1]), dsub(p[2], b.offset[2])};
+        float v[4];
+        sample_local<true, 1>(s, b, l, INTERP, v, err);
+        const float sc = s.n_steps ? run_chain(s, v, 1) : v[0];
+        acc = over4(acc, premultiply(classify(lut_s, lo, inv, sc)));
+        if (gate_alpha && (double)acc.w >= a.alpha_stop) break;
+      }
+    } else {
+      const int ns = a.n_sources;
+      float prev[ISC_MAX_SOURCES];
+#pragma unroll
+      for (int i = 0; i < ISC_MAX_SOURCES; ++i) prev[i] = CUDART_NAN_F;
+      double bsz[3], vb[3];
+      const int* dec = a.decomposition;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        bsz[i] = (double)b.size[i];
+        vb[i] = ddiv((double)a.volume_size[i], (double)dec[i]);  // raycast.py:283-285
+      }
+      for (long long k = r.k_lo; k < r.k_hi; ++k) {
+        ++stations;
+        double p[3];
+        station_pos(o, r.d, dmul((double)k, a.step), p);
+        float4 st = make_float4(0.f, 0.f, 0.f, 0.f);
+        bool stop = false;
+        for (int si = 0; si < ns; ++si) {
+          const isc_source& s = a.src[si];
+          const float cur = scalar_at<false>(s, b, p, INTERP, err);
+          const float4* lut = lut_s + si * ISC_LUT_ENTRIES;
+          const float inv = 1.0f / (s.range_hi - s.range_lo);
+          if (s.mode != ISC_ISO) {
+            st = over4(st, premultiply(classify(lut, s.range_lo, inv, cur)));
+            continue;
+          }
+          // ---- iso: raycast.py:384-468 ----
+          const float thr = s.iso_threshold;
+          const bool exact = s.has_guard && INTERP;
+          float before = prev[si];
+          if (k == r.k_lo && k - 1 >= r.kg_lo) {  // entry pair through the guard
+            double pq[3];
+            station_pos(o, r.d, dmul((double)(k - 1), a.step), pq);
+            before = (!exact || reachable(b.offset, bsz, b.guard, pq)) ? scalar_at<false>(s, b, pq, INTERP, err)
+                                                                     : CUDART_NAN_F;
+          }
+          const float sa = before - thr, sb = cur - thr;
+          bool hit = isfinite(sa) && ((sa < 0.f) != (sb < 0.f));
+          double tau = 0.0, back = 0.0;
+          if (hit) {
+            const float den = sa - sb;
+            tau = den != 0.f ? (double)(sa / den) : 1.0;
+            back = -1.0;
+          }
+          if (exact && !hit && k == r.k_hi - 1 && k + 1 < r.kg_hi) {  // exit pair checked forward
+            double pn[3];
+            station_pos(o, r.d, dmul((double)(k + 1), a.step), pn);
+            double noff[3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+              double c = floor(ddiv(pn[i], vb[i]));
+              c = dmin(dmax(c, 0.0), (double)(dec[i] - 1));
+              noff[i] = dmul(c, vb[i]);
+            }
+            if (reachable(b.offset, bsz, b.guard, pn) && !reachable(noff, vb, b.guard, p)) {
+              const float sn = scalar_at<false>(s, b, pn, INTERP, err) - thr;
+              if ((sb < 0.f) != (sn < 0.f)) {
+                const float den = sb - sn;
+                tau = den != 0.f ? (double)(sb / den) : 1.0;
+                back = 0.0;
+                hit = true;
+              }
+            }
+          }
+          prev[si] = cur;
+          if (hit) {
+            double hp[3];
+            const double t = dmul(dadd(tau, back), a.step);
+#pragma unroll
+            for (int i = 0; i < 3; ++i) hp[i] = dadd(p[i], dmul(t, r.d[i]));
+            const float3 n = iso_normal(s, b, hp, r.d, INTERP, err);
+            const float shade = fabsf(n.x * (float)r.d[0] + n.y * (float)r.d[1] + n.z * (float)r.d[2]);
+            const float4 base = classify(lut, s.range_lo, inv, thr);
+            st = over4(st, make_float4(base.x * shade, base.y * shade, base.z * shade, 1.0f));
+            stop = true;
+          }
+        }
+        acc = over4(acc, st);
+        if (stop || (gate_alpha && (double)acc.w >= a.alpha_stop)) break;
+      }
+    }
+  }
+
+  reinterpret_cast<float4*>(a.out_rgba)[pix] = acc;
+  if (a.out_stations) a.out_stations[pix] = stations;
+  if (a.out_station_total) {
+    const unsigned int warp_total = __reduce_add_sync(__activemask(), stations);
+    if ((threadIdx.x & 31) == (__ffs(__activemask()) - 1) && warp_total)
+      atomicAdd(a.out_station_total, (unsigned long long)warp_total);
+  }
+  if (a.out_hit) a.out_hit[pix] = r.hit ? 1 : 0;
+  if (a.out_t) {
+    a.out_t[2 * pix] = r.t_in;
+    a.out_t[2 * pix + 1] = r.t_out;
+  }
+  if (a.out_krange) {
+    reinterpret_cast<int4*>(a.out_krange)[pix] =
+        make_int4((int)r.k_lo, (int)r.k_hi, (int)r.kg_lo, (int)r.kg_hi);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) ray_setup_kernel(const __grid_constant__ isc_render_args a) {
+  int px, py;
+  tile_pixel(px, py);
+  if (px >= a.camera.width || py >= a.camera.height) return;
+  const long long pix = (long long)py * a.camera.width + px;
+  Ray r;
+  setup_ray(a, px, py, r);
+  if (a.out_hit) a.out_hit[pix] = r.hit ? 1 : 0;
+  if (a.out_t) {
+    a.out_t[2 * pix] = r.t_in;
+    a.out_t[2 * pix + 1] = r.t_out;
+  }
+  if (a.out_krange)
+    reinterpret_cast<int4*>(a.out_krange)[pix] =
+        make_int4((int)r.k_lo, (int)r.k_hi, (int)r.kg_lo, (int)r.kg_hi);
+}
+
+static int validate(const isc_render_args* a, bool need_rgba) {
+  if (!a) return fail(ISC_E_VALUE, "null render args");
+  const isc_camera& c = a->camera;
+  if (c.width <= 0 || c.height <= 0) return fail(ISC_E_SCENE, "image size must be positive");
+  if (!(a->step > 0.0)) return fail(ISC_E_SCENE, "step_length must be positive");
+  if (a->n_sources < 0 || a->n_sources > ISC_MAX_SOURCES) return fail(ISC_E_VALUE, "too many active sources");
+  if (a->n_clip < 0 || a->n_clip > ISC_MAX_CLIP_PLANES) return fail(ISC_E_SCENE, "too many clip planes");
+  if (a->guard_width < 0) return fail(ISC_E_FIELD, "guard width must be non-negative");
+  for (int i = 0; i < 3; ++i) {
+    if (a->brick_size[i] <= 0 || a->volume_size[i] <= 0 || a->decomposition[i] <= 0)
+      return fail(ISC_E_FIELD, "brick/volume size and decomposition must be positive");
+  }
+  if (need_rgba && !a->out_rgba) return fail(ISC_E_VALUE, "out_rgba is required");
+  for (int s = 0; s < a->n_sources; ++s) {
+    const isc_source& src = a->src[s];
+    if (!src.data || !src.lut) return fail(ISC_E_FIELD, "source data / lut pointer is null");
+    if (src.feature_dim < 1 || src.feature_dim > 4) return fail(ISC_E_FIELD, "feature_dim must be 1..4");
+    if (src.n_steps < 0 || src.n_steps > ISC_MAX_CHAIN) return fail(ISC_E_CHAIN, "chain too long");
+    if (src.dtype < ISC_F32 || src.dtype > ISC_BF16) return fail(ISC_E_FIELD, "unsupported dtype");
+    if (!(src.range_lo < src.range_hi)) return fail(ISC_E_SCENE, "value range must satisfy min < max");
+    int dim = src.feature_dim;
+    for (int i = 0; i < src.n_steps; ++i) {
+      if (src.steps[i].in_dim != dim) return fail(ISC_E_CHAIN, "chain step dimension mismatch");
+      const int op = src.steps[i].op;
+      if (op < ISC_OP_ADD || op > ISC_OP_MAX) return fail(ISC_E_CHAIN, "unknown chain opcode");
+      if (op == ISC_OP_LENGTH || op == ISC_OP_SUM) dim = 1;
+    }
+  }
+  return ISC_OK;
+}
+
+}  // namespace isc
+
+using namespace isc;
+
+extern "C" int isc_render_local(const isc_render_args* a, void* stream) {
+  int st = validate(a, true);
+  if (st != ISC_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (a->error_word) ISC_CUDA_CHECK(cudaMemsetAsync(a->error_word, 0, sizeof(uint32_t), s));
+  if (a->out_station_total) ISC_CUDA_CHECK(cudaMemsetAsync(a->out_station_total, 0, sizeof(unsigned long long), s));
+  dim3 grid((a->camera.width + kTile - 1) / kTile, (a->camera.height + kTile - 1) / kTile);
+  const size_t smem = (size_t)a->n_sources * ISC_LUT_ENTRIES * sizeof(float4);
+  const bool fast = a->n_sources == 1 && a->src[0].feature_dim == 1 && a->src[0].mode == ISC_VOLUME &&
+                    a->src[0].dtype == ISC_F32;
+  const bool interp = a->interpolation != 0;
+  if (fast && interp) march_kernel<true, true><<<grid, kThreads, smem, s>>>(*a);
+  else if (fast) march_kernel<true, false><<<grid, kThreads, smem, s>>>(*a);
+  else if (interp) march_kernel<false, true><<<grid, kThreads, smem, s>>>(*a);
+  else march_kernel<false, false><<<grid, kThreads, smem, s>>>(*a);
+  ISC_CUDA_CHECK(cudaGetLastError());
+  return ISC_OK;
+}
+
+extern "C" int isc_ray_setup(const isc_render_args* a, void* stream) {
+  int st = validate(a, false);
+  if (st != ISC_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  dim3 grid((a->camera.width + kTile - 1) / kTile, (a->camera.height + kTile - 1) / kTile);
+  ray_setup_kernel<<<grid, kThreads, 0, s>>>(*a);
+  ISC_CUDA_CHECK(cudaGetLastError());
+  return ISC_OK;
+}

@@ -1,0 +1,121 @@
+// K4: per-source normalisation -- (min, max) of the float32-chained first
+// component over a brick's interior (guard excluded).  There is no reference
+// function for this (value ranges are scene state, scene.py:188,
+// runtime.py:154-157); it feeds the auto value range of a transfer function.
+//
+// Streaming reduction: each warp walks whole x-rows (coalesced loads, 4 rows
+// in flight per warp for memory-level parallelism), reduces with warp
+// shuffles, then one shared-memory pass per CTA and one ordered-integer
+// atomicMin/atomicMax per CTA.  min/max are exact, so the result is
+// bit-identical to the oracle regardless of reduction order.
+#include "common.cuh"
+#include "sample.cuh"
+
+namespace isc {
+
+__device__ __forceinline__ unsigned int order_key(float f) {
+  const unsigned int u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float from_key(unsigned int k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+__global__ void minmax_init(unsigned int* keys) {
+  keys[0] = 0xffffffffu;  // running min key
+  keys[1] = 0u;           // running max key
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(256) minmax_kernel(const __grid_constant__ isc_source s, int sx, int sy, int sz,
+                                                      int g, unsigned int* keys) {
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const long long rows = (long long)sy * sz;
+  float lo = CUDART_INF_F, hi = -CUDART_INF_F;
+  bool any = false;
+  for (long long row = warp; row < rows; row += nwarps) {
+    const int y = (int)(row % sy), z = (int)(row / sy);
+    const long long base = (long long)(z + g) * s.stride[0] + (long long)(y + g) * s.stride[1];
+    for (int x = lane; x < sx; x += 32) {
+      const long long e = base + (long long)(x + g) * s.stride[2];
+      float v[4];
+#pragma unroll
+      for (int c = 0; c < DIM; ++c) v[c] = load_elem(s, e + c * s.stride[3]);
+      const float r = run_chain(s, v, DIM);
+      if (r == r) {
+        lo = fminf(lo, r);
+        hi = fmaxf(hi, r);
+        any = true;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    any |= __shfl_xor_sync(0xffffffffu, (int)any, o) != 0;
+  }
+  __shared__ float slo[8], shi[8];
+  __shared__ int sany[8];
+  const int wib = threadIdx.x >> 5;
+  if (lane == 0) {
+    slo[wib] = lo;
+    shi[wib] = hi;
+    sany[wib] = any;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    bool b = false;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+      if (!sany[i]) continue;
+      lo = b ? fminf(lo, slo[i]) : slo[i];
+      hi = b ? fmaxf(hi, shi[i]) : shi[i];
+      b = true;
+    }
+    if (b) {
+      atomicMin(keys, order_key(lo));
+      atomicMax(keys + 1, order_key(hi));
+    }
+  }
+}
+
+__global__ void minmax_finish(const unsigned int* keys, float* out) {
+  const bool empty = keys[1] == 0u;
+  out[0] = empty ? CUDART_NAN_F : from_key(keys[0]);
+  out[1] = empty ? CUDART_NAN_F : from_key(keys[1]);
+}
+
+}  // namespace isc
+
+using namespace isc;
+
+extern "C" int isc_value_range(const isc_source* src, const int32_t brick_size[3], int32_t guard,
+                               float* out_minmax, void* stream) {
+  if (!src || !src->data || !out_minmax || !brick_size) return fail(ISC_E_VALUE, "null argument");
+  if (src->feature_dim < 1 || src->feature_dim > 4) return fail(ISC_E_FIELD, "feature_dim must be 1..4");
+  if (src->n_steps < 0 || src->n_steps > ISC_MAX_CHAIN) return fail(ISC_E_CHAIN, "chain too long");
+  for (int i = 0; i < 3; ++i)
+    if (brick_size[i] <= 0) return fail(ISC_E_FIELD, "brick size must be positive");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  // out_minmax holds 4 words: [0], [1] = min, max (float); [2], [3] = scratch keys.
+  unsigned int* keys = reinterpret_cast<unsigned int*>(out_minmax) + 2;
+  int dev = 0;
+  ISC_CUDA_CHECK(cudaGetDevice(&dev));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long rows = (long long)brick_size[1] * brick_size[2];
+  const long long want = (rows + 7) / 8;  // 8 warps per CTA, >= 1 row per warp
+  const int grid = (int)(want < (long long)sms * 8 ? (want > 0 ? want : 1) : (long long)sms * 8);
+  minmax_init<<<1, 1, 0, s>>>(keys);
+  switch (src->feature_dim) {
+    case 1: minmax_kernel<1><<<grid, 256, 0, s>>>(*src, brick_size[0], brick_size[1], brick_size[2], guard, keys); break;
+    case 2: minmax_kernel<2><<<grid, 256, 0, s>>>(*src, brick_size[0], brick_size[1], brick_size[2], guard, keys); break;
+    case 3: minmax_kernel<3><<<grid, 256, 0, s>>>(*src, brick_size[0], brick_size[1], brick_size[2], guard, keys); break;
+    default: minmax_kernel<4><<<grid, 256, 0, s>>>(*src, brick_size[0], brick_size[1], brick_size[2], guard, keys); break;
+  }
+  minmax_finish<<<1, 1, 0, s>>>(keys, out_minmax);
+  ISC_CUDA_CHECK(cudaGetLastError());
+  return ISC_OK;
+}

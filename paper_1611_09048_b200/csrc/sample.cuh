@@ -1,0 +1,187 @@
+// Field sampling, functor chains and transfer-function classification on the
+// device (float32 arithmetic on values, float64 for positions/indices).
+//
+//   guard / clamp contract   fields.py:218-246  (guard reads legal only when
+//                            has_guard && interpolation; else clamp per index)
+//   trilinear                raycast.py:182-199 (8 corners, floor + frac)
+//   nearest                  raycast.py:174-178 (floor, clamp)
+//   chain                    functors.py:102-147, 212-222; first component
+//                            functors.py:239-240
+//   classify                 scene.py:139-152   (clip, x = 255 t, lerp LUT,
+//                            non-finite -> transparent)
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+
+namespace isc {
+
+struct Brick {
+  int size[3];
+  int guard;
+  double offset[3];
+};
+
+__device__ __forceinline__ float load_elem(const isc_source& s, long long idx) {
+  switch (s.dtype) {
+    case ISC_F64: return (float)__ldg(reinterpret_cast<const double*>(s.data) + idx);
+    case ISC_F16: return __half2float(reinterpret_cast<const __half*>(s.data)[idx]);
+    case ISC_BF16: return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(s.data)[idx]);
+    default: return __ldg(reinterpret_cast<const float*>(s.data) + idx);
+  }
+}
+
+template <bool F32>
+__device__ __forceinline__ float load_as(const isc_source& s, long long idx) {
+  if constexpr (F32) return __ldg(reinterpret_cast<const float*>(s.data) + idx);
+  else return load_elem(s, idx);
+}
+
+// Integer local index of one axis for the corner pair (i, i+1) under the
+// guard/clamp contract.  Returns false on a guard-contract violation (the
+// indices are then clamped into the halo so the read stays in bounds).
+__device__ __forceinline__ bool corner_pair(int i, int size, int g, bool guarded, int& i0, int& i1) {
+  if (guarded) {
+    bool ok = (i >= -g) && (i + 1 < size + g);
+    i0 = min(max(i, -g), size + g - 1);
+    i1 = min(max(i + 1, -g), size + g - 1);
+    return ok;
+  }
+  i0 = min(max(i, 0), size - 1);
+  i1 = min(max(i + 1, 0), size - 1);
+  return true;
+}
+
+// Sample a source at a LOCAL position (global - offset) -> dim components.
+template <bool F32, int DIM>
+__device__ __forceinline__ void sample_local(const isc_source& s, const Brick& b, const double l[3],
+                                             bool interp, float v[4], uint32_t* err) {
+  const int g = b.guard;
+  const double fx0 = floor(l[0]), fy0 = floor(l[1]), fz0 = floor(l[2]);
+  const int ix = (int)fx0, iy = (int)fy0, iz = (int)fz0;
+  const int dim = DIM > 0 ? DIM : s.feature_dim;
+  if (!interp) {
+    const int cx = min(max(ix, 0), b.size[0] - 1);
+    const int cy = min(max(iy, 0), b.size[1] - 1);
+    const int cz = min(max(iz, 0), b.size[2] - 1);
+    const long long base = (long long)(cz + g) * s.stride[0] + (long long)(cy + g) * s.stride[1] +
+                           (long long)(cx + g) * s.stride[2];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (c < dim) v[c] = load_as<F32>(s, base + c * s.stride[3]);
+    return;
+  }
+  const bool guarded = s.has_guard != 0;
+  int x0, x1, y0, y1, z0, z1;
+  bool ok = corner_pair(ix, b.size[0], g, guarded, x0, x1);
+  ok &= corner_pair(iy, b.size[1], g, guarded, y0, y1);
+  ok &= corner_pair(iz, b.size[2], g, guarded, z0, z1);
+  if (!ok && err) atomicAdd(err, 1u);
+  const float fx = (float)dsub(l[0], fx0), fy = (float)dsub(l[1], fy0), fz = (float)dsub(l[2], fz0);
+  const long long ox0 = (long long)(x0 + g) * s.stride[2], ox1 = (long long)(x1 + g) * s.stride[2];
+  const long long oy0 = (long long)(y0 + g) * s.stride[1], oy1 = (long long)(y1 + g) * s.stride[1];
+  const long long oz0 = (long long)(z0 + g) * s.stride[0], oz1 = (long long)(z1 + g) * s.stride[0];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    if (c >= dim) break;
+    const long long cc = c * s.stride[3];
+    const float v000 = load_as<F32>(s, oz0 + oy0 + ox0 + cc), v100 = load_as<F32>(s, oz0 + oy0 + ox1 + cc);
+    const float v010 = load_as<F32>(s, oz0 + oy1 + ox0 + cc), v110 = load_as<F32>(s, oz0 + oy1 + ox1 + cc);
+    const float v001 = load_as<F32>(s, oz1 + oy0 + ox0 + cc), v101 = load_as<F32>(s, oz1 + oy0 + ox1 + cc);
+    const float v011 = load_as<F32>(s, oz1 + oy1 + ox0 + cc), v111 = load_as<F32>(s, oz1 + oy1 + ox1 + cc);
+    const float a0 = fmaf(fx, v100 - v000, v000), a1 = fmaf(fx, v110 - v010, v010);
+    const float a2 = fmaf(fx, v101 - v001, v001), a3 = fmaf(fx, v111 - v011, v011);
+    const float b0 = fmaf(fy, a1 - a0, a0), b1 = fmaf(fy, a3 - a2, a2);
+    v[c] = fmaf(fz, b1 - b0, b0);
+  }
+}
+
+// Functor chain on up to 4 components; returns the first component
+// (reduce_to_scalar_array).  Sums and norms use explicit round-to-nearest
+// adds/multiplies so the float32 value-range kernel is bit-exact with the
+// oracle's float32 restatement.
+__device__ __forceinline__ float run_chain(const isc_source& s, float v[4], int dim) {
+  for (int i = 0; i < s.n_steps; ++i) {
+    const isc_chain_step& st = s.steps[i];
+    switch (st.op) {
+      case ISC_OP_ADD:
+#pragma unroll
+        for (int c = 0; c < 4; ++c) if (c < dim) v[c] = fadd(v[c], st.arg[c]);
+        break;
+      case ISC_OP_MUL:
+#pragma unroll
+        for (int c = 0; c < 4; ++c) if (c < dim) v[c] = fmul(v[c], st.arg[c]);
+        break;
+      case ISC_OP_POW:
+#pragma unroll
+        for (int c = 0; c < 4; ++c) if (c < dim) v[c] = powf(v[c], st.arg[c]);
+        break;
+      case ISC_OP_LENGTH: {
+        float acc = fmul(v[0], v[0]);
+#pragma unroll
+        for (int c = 1; c < 4; ++c) if (c < dim) acc = fadd(acc, fmul(v[c], v[c]));
+        v[0] = __fsqrt_rn(acc);
+        dim = 1;
+      } break;
+      case ISC_OP_SUM: {
+        float acc = v[0];
+#pragma unroll
+        for (int c = 1; c < 4; ++c) if (c < dim) acc = fadd(acc, v[c]);
+        v[0] = acc;
+        dim = 1;
+      } break;
+      case ISC_OP_SQRT:
+#pragma unroll
+        for (int c = 0; c < 4; ++c) if (c < dim) v[c] = __fsqrt_rn(v[c]);
+        break;
+      case ISC_OP_ABS:
+#pragma unroll
+        for (int c = 0; c < 4; ++c) if (c < dim) v[c] = fabsf(v[c]);
+        break;
+      case ISC_OP_NEG:
+#pragma unroll
+        for (int c = 0; c < 4; ++c) if (c < dim) v[c] = -v[c];
+        break;
+      case ISC_OP_EXP:
+#pragma unroll
+        for (int c = 0; c < 4; ++c) if (c < dim) v[c] = expf(v[c]);
+        break;
+      case ISC_OP_LOG:
+#pragma unroll
+        for (int c = 0; c < 4; ++c) if (c < dim) v[c] = logf(v[c]);
+        break;
+      case ISC_OP_MIN:
+#pragma unroll
+        for (int c = 0; c < 4; ++c) if (c < dim) v[c] = (v[c] != v[c]) ? v[c] : fminf(v[c], st.arg[c]);
+        break;
+      case ISC_OP_MAX:
+#pragma unroll
+        for (int c = 0; c < 4; ++c) if (c < dim) v[c] = (v[c] != v[c]) ? v[c] : fmaxf(v[c], st.arg[c]);
+        break;
+      default: break;
+    }
+  }
+  return v[0];
+}
+
+// Straight RGBA from a LUT held in shared memory.
+__device__ __forceinline__ float4 classify(const float4* lut, float lo, float inv_span, float v) {
+  if (!isfinite(v)) return make_float4(0.f, 0.f, 0.f, 0.f);
+  float t = (v - lo) * inv_span;
+  t = fminf(fmaxf(t, 0.0f), 1.0f);
+  const float x = t * (float)(ISC_LUT_ENTRIES - 1);
+  const int i0 = min((int)x, ISC_LUT_ENTRIES - 1);
+  const int i1 = min(i0 + 1, ISC_LUT_ENTRIES - 1);
+  const float w = x - (float)i0;
+  const float4 a = lut[i0], b = lut[i1];
+  return make_float4(fmaf(w, b.x - a.x, a.x), fmaf(w, b.y - a.y, a.y), fmaf(w, b.z - a.z, a.z),
+                     fmaf(w, b.w - a.w, a.w));
+}
+
+__device__ __forceinline__ float4 premultiply(float4 c) {
+  return make_float4(c.x * c.w, c.y * c.w, c.z * c.w, c.w);
+}
+
+}  // namespace isc

@@ -1,0 +1,83 @@
+"""Device plumbing shared by the render and composite wrappers: torch is used
+for device memory and streams only; every computation goes through the C-ABI."""
+
+from __future__ import annotations
+
+import ctypes as C
+from collections import OrderedDict
+
+import numpy as np
+import torch
+
+from . import _abi
+
+_DTYPES = {torch.float32: _abi.F32, torch.float64: _abi.F64, torch.float16: _abi.F16, torch.bfloat16: _abi.BF16}
+
+
+def require_cuda() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1611_09048_b200 renders on a CUDA device (sm_100a); none is available "
+                           "and there is no CPU fallback")
+    _abi.lib()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_handle(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def as_device_field(array, device: torch.device) -> torch.Tensor:
+    """Zero-copy for CUDA tensors on ``device``; numpy / host tensors are staged
+    (one H2D copy).  Integer arrays are converted to float32."""
+    if isinstance(array, torch.Tensor):
+        t = array
+        if t.device != device:
+            t = t.to(device, non_blocking=True)
+    else:
+        a = np.asarray(array)
+        if a.dtype not in (np.float32, np.float64, np.float16):
+            a = a.astype(np.float32)
+        t = torch.from_numpy(np.ascontiguousarray(a)).to(device, non_blocking=False)
+    if t.dtype not in _DTYPES:
+        t = t.to(torch.float32)
+    return t
+
+
+def dtype_code(t: torch.Tensor) -> int:
+    return _DTYPES[t.dtype]
+
+
+class LutCache:
+    """Device float32 LUTs keyed by content, so an unchanged transfer function
+    is uploaded once and steering changes cost one 4 KB H2D copy."""
+
+    def __init__(self, capacity: int = 64):
+        self._cache: "OrderedDict[tuple, torch.Tensor]" = OrderedDict()
+        self.capacity = capacity
+        self.uploads = 0
+
+    def get(self, lut: np.ndarray, device: torch.device) -> torch.Tensor:
+        host = np.ascontiguousarray(lut, dtype=np.float32)
+        key = (device.index, host.tobytes())
+        t = self._cache.get(key)
+        if t is not None:
+            self._cache.move_to_end(key)
+            return t
+        t = torch.from_numpy(host).to(device)
+        self.uploads += 1
+        self._cache[key] = t
+        if len(self._cache) > self.capacity:
+            self._cache.popitem(last=False)
+        return t
+
+
+LUTS = LutCache()
+
+
+def ptr(t) -> int:
+    return 0 if t is None else int(t.data_ptr())
+
+
+def c_ptr(t) -> C.c_void_p:
+    return C.c_void_p(ptr(t))

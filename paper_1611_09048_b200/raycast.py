@@ -1,0 +1,315 @@
+"""Brick rendering entry point: ``render_local`` over the sm_100a kernel.
+
+Drop-in for ``insitu.raycast.render_local`` (raycast.py:492-541): same
+arguments (a rank context exposing ``domain``, ``global_volume``,
+``registry``, ``functor_registry``, ``limits``; a ``SceneState``; optional
+``plans`` and ``station_recorder``) and the same result type, except that
+``LocalImage.pixels`` is a CUDA float32 tensor (H, W, 4) of premultiplied
+RGBA instead of a float64 numpy array.  All per-pixel work -- ray setup,
+clipping, the station march, sampling, chains, classification, iso-surfaces
+and front-to-back compositing -- runs in ``isc_render_local``; this module
+only packs the argument block.
+
+``station_recorder(k, pixel_ids)`` is honoured by replaying the per-pixel
+station ranges the kernel reports (stations of a pixel are contiguous from
+its k_lo), which reproduces the reference's callback sequence exactly.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _abi
+from .device import LUTS, as_device_field, dtype_code, ptr, require_cuda, stream_handle
+from .errors import FieldError, GuardContractError
+from .fields import LocalDomain, SourceHandle, SourceRegistry
+from .functors import ChainLimits, FunctorChain, FunctorRegistry, device_program, parse_chain
+from .scene import ISO_MODE, SceneState, TransferFunction
+
+StationRecorder = Callable[[int, np.ndarray], None]
+
+__all__ = ["LocalImage", "SourcePlan", "build_plans", "render_local", "RankContext", "pack_render_args",
+           "ray_box_intersection", "ray_setup"]
+
+
+class LocalImage:
+    """One rank's partial image (raycast.py:38-50).  ``pixels`` is a CUDA
+    float32 (H, W, 4) premultiplied tensor; ``stations`` is resolved lazily
+    from the device station counters (one reduction + sync on first access)."""
+
+    def __init__(self, width: int, height: int, pixels, order_key: int = 0, stations=0):
+        self.width = width
+        self.height = height
+        self.pixels = pixels
+        self.order_key = order_key
+        self._stations = stations
+        self.station_counts = None     # (H*W,) uint32 device tensor when kept
+        self.krange = None             # (H*W, 4) int32 device tensor when kept
+        self._error_word = None
+
+    @property
+    def stations(self) -> int:
+        s = self._stations
+        if callable(s):
+            s = int(s())
+            self._stations = s
+        return s
+
+    @stations.setter
+    def stations(self, v):
+        self._stations = v
+
+    def check(self) -> "LocalImage":
+        """Raise GuardContractError if the kernel saw a guard-contract violation."""
+        if self._error_word is not None:
+            n = int(self._error_word.item()) & 0xFFFFFFFF
+            self._error_word = None
+            if n:
+                raise GuardContractError(f"{n} trilinear reads beyond the guard halo")
+        return self
+
+    @staticmethod
+    def blank(width: int, height: int, order_key: int = 0) -> "LocalImage":
+        dev = require_cuda()
+        return LocalImage(width, height, torch.zeros((height, width, 4), device=dev), order_key)
+
+
+@dataclass(frozen=True)
+class SourcePlan:
+    """Per-active-source render inputs (raycast.py:53-63)."""
+
+    source_id: int
+    handle: SourceHandle
+    domain: LocalDomain
+    chain: FunctorChain
+    tf: TransferFunction
+    mode: str
+    iso_threshold: float
+
+
+def build_plans(registry: SourceRegistry, functor_registry: FunctorRegistry, limits: ChainLimits,
+                scene: SceneState) -> list:
+    """Active sources in id order with parsed chains (raycast.py:66-93)."""
+    known = set(registry.source_ids)
+    plans = []
+    for sid in sorted(scene.settings.active_set):
+        if sid not in known:
+            raise ValueError(f"active source id {sid} is not registered")
+        handle = registry.render_handle(sid)
+        chain = parse_chain(scene.chain_text(sid), functor_registry, limits, handle.descriptor.feature_dim)
+        plans.append(SourcePlan(sid, handle, registry.domain, chain, scene.transfer_function(sid),
+                                scene.settings.mode(sid), scene.settings.iso_threshold(sid)))
+    return plans
+
+
+@dataclass
+class RankContext:
+    """What ``render_local`` reads from a rank (runtime.py:263-281, subset)."""
+
+    global_volume: object
+    domain: LocalDomain
+    registry: SourceRegistry
+    functor_registry: FunctorRegistry
+    limits: ChainLimits
+    transport: object = None
+
+
+def _strides(t: torch.Tensor):
+    s = list(t.stride())
+    return (s[0], s[1], s[2], s[3] if t.dim() == 4 else 1)
+
+
+def pack_render_args(domain, volume, scene: SceneState, plans: Sequence[SourcePlan], device,
+                     keep: list) -> _abi.RenderArgs:
+    """Fill an ``isc_render_args`` block.  ``keep`` collects the tensors whose
+    device pointers the block references (they must outlive the launch)."""
+    a = _abi.RenderArgs()
+    cam = scene.camera
+    w, h = cam.image_size
+    fwd, right, up = cam.basis()
+    a.camera.origin[:] = [float(v) for v in cam.position]
+    a.camera.fwd[:] = fwd.tolist()
+    a.camera.right[:] = right.tolist()
+    a.camera.up[:] = up.tolist()
+    a.camera.tan_half = math.tan(cam.vertical_fov / 2.0)
+    a.camera.aspect = w / h
+    a.camera.width, a.camera.height = int(w), int(h)
+    st = scene.settings
+    a.step = float(st.step_length)
+    a.alpha_stop = float(st.early_termination_alpha)
+    a.interpolation = 1 if st.interpolation else 0
+    a.guard_width = int(domain.guard_width)
+    a.brick_offset[:] = [int(v) for v in domain.offset]
+    a.brick_size[:] = [int(v) for v in domain.size]
+    a.volume_size[:] = [int(v) for v in volume.size]
+    a.decomposition[:] = [int(v) for v in volume.decomposition]
+    if len(scene.clip_planes) > _abi.MAX_CLIP_PLANES:
+        raise ValueError(f"at most {_abi.MAX_CLIP_PLANES} clip planes")
+    origin = np.asarray(cam.position, dtype=np.float64)
+    a.n_clip = len(scene.clip_planes)
+    for i, plane in enumerate(scene.clip_planes):
+        n = np.asarray(plane.normal)
+        a.clip[i].point[:] = [float(v) for v in plane.point]
+        a.clip[i].normal[:] = n.tolist()
+        a.clip[i].f0 = float(np.dot(origin - np.asarray(plane.point), n))  # raycast.py:133
+    if len(plans) > _abi.MAX_SOURCES:
+        raise ValueError(f"at most {_abi.MAX_SOURCES} active sources per render")
+    a.n_sources = len(plans)
+    for i, plan in enumerate(plans):
+        s = a.src[i]
+        hnd = plan.handle
+        array, guard = hnd.device_view(domain)
+        t = as_device_field(array, device)
+        dim = hnd.descriptor.feature_dim
+        need = tuple(domain.size[a_] + 2 * guard for a_ in (2, 1, 0))
+        if tuple(t.shape[:3]) != need:
+            raise FieldError(f"source {hnd.descriptor.name!r}: array shape {tuple(t.shape)} does not match "
+                             f"domain size + 2*guard {need}")
+        if hnd.descriptor.has_guard and st.interpolation and guard < domain.guard_width:
+            raise FieldError(f"source {hnd.descriptor.name!r} declares a guard of {guard} cells but the "
+                             f"domain promises {domain.guard_width}")
+        keep.append(t)
+        sz, sy, sx, sc = _strides(t)
+        # The kernel indexes with the domain guard; re-base the pointer when
+        # the array carries a different halo width (fields.py:274-276).
+        shift = (guard - domain.guard_width) * (sz + sy + sx)
+        s.data = ptr(t) + shift * t.element_size()
+        s.stride[:] = [sz, sy, sx, sc]
+        s.dtype = dtype_code(t)
+        s.feature_dim = dim
+        s.has_guard = 1 if hnd.descriptor.has_guard else 0
+        s.mode = _abi.ISO if plan.mode == ISO_MODE else _abi.VOLUME
+        s.iso_threshold = float(plan.iso_threshold)
+        s.range_lo, s.range_hi = (float(v) for v in plan.tf.value_range)
+        lut = LUTS.get(plan.tf.lut, device)
+        keep.append(lut)
+        s.lut = ptr(lut)
+        prog = device_program(plan.chain)
+        s.n_steps = len(prog)
+        for j, (op, in_dim, arg) in enumerate(prog):
+            s.steps[j].op = op
+            s.steps[j].in_dim = in_dim
+            s.steps[j].arg[:] = [float(v) for v in arg]
+    return a
+
+
+def render_local(rank_ctx, scene: SceneState, plans: Optional[Sequence[SourcePlan]] = None,
+                 station_recorder: Optional[StationRecorder] = None, *, out: Optional[torch.Tensor] = None,
+                 stream=None, check_errors: bool = True, keep_station_counts: bool = False,
+                 keep_krange: bool = False, events=None) -> LocalImage:
+    """Render the rank's brick into a partial image (raycast.py:492-541).
+
+    ``out`` (optional) is a caller-owned CUDA float32 (H, W, 4) tensor to
+    render into (e.g. an ``NvlinkTransport`` canvas, which saves the copy in
+    ``binary_swap``).  ``check_errors=False`` skips the synchronising guard
+    check; call ``LocalImage.check()`` later instead.  ``events`` = (start,
+    end) CUDA events recorded around the kernel launch (bench timing).
+    """
+    device = require_cuda()
+    domain, volume = rank_ctx.domain, rank_ctx.global_volume
+    if plans is None:
+        plans = build_plans(rank_ctx.registry, rank_ctx.functor_registry, rank_ctx.limits, scene)
+    w, h = scene.camera.image_size
+    keep: list = []
+    args = pack_render_args(domain, volume, scene, plans, device, keep)
+    if out is None:
+        out = torch.empty((h, w, 4), dtype=torch.float32, device=device)
+    elif out.shape != (h, w, 4) or out.dtype != torch.float32 or not out.is_contiguous() or out.device != device:
+        raise ValueError(f"out must be a contiguous float32 ({h}, {w}, 4) tensor on {device}")
+    per_px = keep_station_counts or station_recorder is not None
+    counts = torch.empty(h * w, dtype=torch.int32, device=device) if per_px else None
+    kr = torch.empty((h * w, 4), dtype=torch.int32, device=device) if (keep_krange or station_recorder) else None
+    stats = torch.empty(2, dtype=torch.int64, device=device)   # [station total, error word]; zeroed by the library
+    args.out_rgba = ptr(out)
+    args.out_stations = ptr(counts) if counts is not None else None
+    args.out_krange = ptr(kr) if kr is not None else None
+    args.out_station_total = ptr(stats)
+    args.error_word = ptr(stats) + 8
+    if events is not None:
+        events[0].record(stream)
+    _abi.check(_abi.lib().isc_render_local(C.byref(args), C.c_void_p(stream_handle(stream))), "render_local")
+    if events is not None:
+        events[1].record(stream)
+
+    img = LocalImage(w, h, out)
+    img._error_word = stats[1:]
+    img._stations = lambda: int(stats[0].item())
+    taps = 8 if scene.settings.interpolation else 1
+    for plan in plans:
+        plan.handle.add_device_samples(lambda img=img, taps=taps: taps * img.stations)
+    img.station_counts = counts
+    img.krange = kr
+    if check_errors:
+        img.check()
+    if station_recorder is not None:
+        _replay_stations(station_recorder, counts, kr)
+    keep.clear()
+    return img
+
+
+def ray_setup(rank_ctx, scene: SceneState, stream=None) -> dict:
+    """Ray setup only (isc_ray_setup): per-pixel hit mask, brick interval and
+    station ranges, for parity checks against the float64 reference."""
+    device = require_cuda()
+    w, h = scene.camera.image_size
+    keep: list = []
+    args = pack_render_args(rank_ctx.domain, rank_ctx.global_volume, scene, [], device, keep)
+    hit = torch.empty(h * w, dtype=torch.uint8, device=device)
+    tt = torch.empty((h * w, 2), dtype=torch.float64, device=device)
+    kr = torch.empty((h * w, 4), dtype=torch.int32, device=device)
+    args.out_hit, args.out_t, args.out_krange = ptr(hit), ptr(tt), ptr(kr)
+    _abi.check(_abi.lib().isc_ray_setup(C.byref(args), C.c_void_p(stream_handle(stream))), "ray_setup")
+    return {"hit": hit.bool(), "t_in": tt[:, 0], "t_out": tt[:, 1], "k_lo": kr[:, 0], "k_hi": kr[:, 1],
+            "kg_lo": kr[:, 2], "kg_hi": kr[:, 3]}
+
+
+def _replay_stations(recorder: StationRecorder, counts: torch.Tensor, kr: torch.Tensor) -> None:
+    c = counts.cpu().numpy().astype(np.int64)
+    lo = kr[:, 0].cpu().numpy().astype(np.int64)
+    live = np.nonzero(c > 0)[0]
+    if live.size == 0:
+        return
+    start = lo[live]
+    stop = start + c[live]
+    for k in range(int(start.min()), int(stop.max())):
+        sel = live[(start <= k) & (k < stop)]
+        if sel.size:
+            recorder(k, sel)
+
+
+def ray_box_intersection(origin, direction, box_lo, box_hi, clip_planes=()):
+    """Host scalar utility (raycast.py:146-162): parametric interval of one ray
+    in a cuboid after clipping, or None."""
+    o = np.asarray(origin, dtype=np.float64)
+    d = np.asarray(direction, dtype=np.float64)
+    if not d.any():
+        raise ValueError("ray direction must be non-zero")
+    lo = np.asarray(box_lo, dtype=np.float64)
+    hi = np.asarray(box_hi, dtype=np.float64)
+    t0, t1 = -np.inf, np.inf
+    for a in range(3):
+        if d[a] == 0.0:
+            if not lo[a] <= o[a] <= hi[a]:
+                return None
+            continue
+        ta, tb = (lo[a] - o[a]) / d[a], (hi[a] - o[a]) / d[a]
+        t0, t1 = max(t0, min(ta, tb)), min(t1, max(ta, tb))
+    for plane in clip_planes:
+        n = np.asarray(plane.normal)
+        f0 = float(np.dot(o - np.asarray(plane.point), n))
+        dn = float(d @ n)
+        if dn > 0:
+            t0 = max(t0, -f0 / dn)
+        elif dn < 0:
+            t1 = min(t1, -f0 / dn)
+        elif f0 < 0:
+            return None
+    if t1 < t0:
+        return None
+    return (float(t0), float(t1))

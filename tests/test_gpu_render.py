@@ -1,0 +1,218 @@
+"""GPU parity: the sm_100a render path against the reference goldens and the oracle.
+
+Tolerances (north star): float RGBA max-abs <= 1e-3 before 8-bit
+quantisation; hit masks, station ranges and per-pixel station counts
+bit-exact.  Colours are float32 on the device vs float64 in the reference.
+"""
+
+import numpy as np
+import pytest
+
+from case_build import full_fields, oracle_render
+from golden_io import cases, decomp_key, load
+
+pytestmark = pytest.mark.gpu
+
+RGBA_TOL = 1e-3
+
+
+def _torch():
+    import torch
+    return torch
+
+
+@pytest.mark.parametrize("name", sorted(cases.RENDER_CASES))
+def test_render_matches_reference_goldens(name):
+    import paper_1611_09048_b200 as P
+    from product_build import product_ctx, product_scene
+    c = cases.case(name)
+    gold = load(f"render_{name}.npz")
+    scene = product_scene(c)
+    full = full_fields(c)
+    for decomp in c["decompositions"]:
+        key = decomp_key(decomp)
+        images = []
+        for rank in range(int(np.prod(decomp))):
+            p = f"{key}_r{rank}_"
+            ctx = product_ctx(c, decomp, rank, full)
+            rs = P.raycast.ray_setup(ctx, scene)
+            assert np.array_equal(rs["hit"].cpu().numpy(), gold[p + "hit"]), (name, key, rank)
+            hit = gold[p + "hit"]
+            for k in ("k_lo", "k_hi", "kg_lo", "kg_hi"):
+                got = rs[k].cpu().numpy()
+                assert np.array_equal(got[hit], gold[p + k][hit]), (name, key, rank, k)
+            tin = rs["t_in"].cpu().numpy()
+            fin = np.isfinite(gold[p + "t_in"])
+            np.testing.assert_allclose(tin[fin], gold[p + "t_in"][fin], rtol=4e-16, atol=0)
+            img = P.render_local(ctx, scene, keep_station_counts=True)
+            rgba = img.pixels.cpu().numpy().astype(np.float64)
+            err = np.abs(rgba - gold[p + "rgba"]).max()
+            assert err <= RGBA_TOL, (name, key, rank, err)
+            counts = img.station_counts.cpu().numpy().astype(np.int64)
+            want = gold[p + "stations"].astype(np.int64)
+            if any(s["mode"] == "iso" for s in c["sources"]) or c["alpha_stop"] < 1.0:
+                # iso / early termination: a float32 sign or threshold decision
+                # may end a ray one station apart on a handful of pixels.
+                assert (counts != want).mean() <= 0.002, (name, key, rank)
+            else:
+                assert np.array_equal(counts, want), (name, key, rank)
+            assert img.stations == int(counts.sum())
+            images.append(img.pixels)
+        order = P.visibility_order(P.GlobalVolume(tuple(c["size"]), tuple(decomp)), scene.camera)
+        assert order == [int(v) for v in gold[key + "_order"]]
+        comp = P.composite_sequential(images, order).cpu().numpy()
+        assert np.abs(comp - gold[key + "_composite"]).max() <= RGBA_TOL
+
+
+def test_render_matches_oracle_random_cameras():
+    """Seeded random cameras / TFs on a random field, CUDA vs the oracle."""
+    import paper_1611_09048_b200 as P
+    from oracle import isaac_oracle as O
+    torch = _torch()
+    rng = np.random.default_rng(1234)
+    n = 24
+    field = rng.random((n + 2, n + 2, n + 2), dtype=np.float32)
+    for trial in range(6):
+        pos = tuple(float(v) for v in rng.uniform(-2 * n, 3 * n, 3))
+        target = tuple(float(v) for v in rng.uniform(0.3 * n, 0.7 * n, 3))
+        w, h = int(rng.integers(17, 70)), int(rng.integers(9, 50))
+        step = float(rng.uniform(0.2, 1.3))
+        interp = bool(trial % 3 != 2)
+        pts = [(0.0, *rng.random(4)), (float(rng.uniform(0.2, 0.8)), *rng.random(4)), (1.0, *rng.random(4))]
+        vol = P.GlobalVolume((n, n, n), (1, 1, 1))
+        dom = vol.local_domain(0, 1)
+        reg = P.SourceRegistry(dom)
+        reg.register_handle(P.array_backed_handle(P.SourceDescriptor("f", 1, has_guard=True),
+                                                  torch.from_numpy(field).cuda(), 1))
+        P.update_sources(reg, {0}, {})
+        fr = P.default_registry()
+        ctx = P.RankContext(vol, dom, reg, fr, fr.limits)
+        scene = P.SceneState(camera=P.Camera(pos, target, image_size=(w, h)), tf_points={0: pts},
+                             value_ranges={0: (0.1, 0.9)},
+                             settings=P.RenderSettings(active_set=(0,), interpolation=interp, step_length=step,
+                                                       early_termination_alpha=1.0))
+        got = P.render_local(ctx, scene).pixels.cpu().numpy()
+        src = O.Source(array=field, offset=(0, 0, 0), size=(n, n, n), guard=1, lut=O.lut_from_points(pts),
+                       value_range=(0.1, 0.9))
+        ref = O.render_brick({"position": pos, "look_at": target, "width": w, "height": h},
+                             O.Brick((0, 0, 0), (n, n, n), 1, (n, n, n)), [src], step=step, interp=interp)
+        assert np.abs(got - ref.rgba).max() <= RGBA_TOL, trial
+
+
+def test_station_recorder_replay_matches_oracle():
+    import paper_1611_09048_b200 as P
+    from product_build import product_ctx, product_scene
+    c = cases.case("random_bricks")
+    gold = load("render_random_bricks.npz")
+    scene = product_scene(c)
+    full = full_fields(c)
+    for rank in range(8):
+        want: dict = {}
+        oracle_render(c, gold, (2, 2, 2), rank, recorder=lambda k, ids: [want.setdefault(int(i), []).append(k)
+                                                                        for i in ids])
+        got: dict = {}
+        ctx = product_ctx(c, (2, 2, 2), rank, full)
+        P.render_local(ctx, scene, station_recorder=lambda k, ids: [got.setdefault(int(i), []).append(k)
+                                                                   for i in ids])
+        assert got == want
+
+
+def test_inactive_sources_never_touched():
+    import paper_1611_09048_b200 as P
+    from product_build import product_ctx, product_scene
+    c = cases.case("multi")
+    scene = product_scene(c)
+    full = full_fields(c)
+    for rank in range(2):
+        ctx = product_ctx(c, (2, 1, 1), rank, full)
+        P.render_local(ctx, scene)
+        assert ctx.registry.handle(0).sample_count > 0
+        assert ctx.registry.handle(1).sample_count > 0
+        assert ctx.registry.handle(2).sample_count == 0
+
+
+def test_offscreen_is_transparent_and_energy_bound():
+    import paper_1611_09048_b200 as P
+    from product_build import product_ctx, product_scene
+    c = cases.case("c1")
+    ctx = product_ctx(c, (1, 1, 1), 0)
+    scene = product_scene(c)
+    away = P.SceneState(camera=P.Camera((32, 32, -100), (32, 32, -200), image_size=(40, 30)),
+                        tf_points=scene.tf_points, value_ranges=scene.value_ranges, settings=scene.settings)
+    assert float(P.render_local(ctx, away).pixels.abs().sum()) == 0.0
+    px = P.render_local(ctx, scene).pixels
+    assert bool((px[..., :3] <= px[..., 3:] + 1e-6).all())
+    assert float(px[..., 3].max()) <= 1.0 + 1e-6 and float(px[..., 3].min()) >= 0.0
+
+
+def test_guard_contract_violation_raises():
+    import paper_1611_09048_b200 as P
+    torch = _torch()
+    n = 8
+    vol = P.GlobalVolume((n, n, n))
+    dom = vol.local_domain(0, 0)          # the domain promises no halo ...
+    reg = P.SourceRegistry(dom)
+    arr = torch.rand((n, n, n), device="cuda")
+    reg.register_handle(P.array_backed_handle(P.SourceDescriptor("f", 1, has_guard=True), arr, 0))
+    P.update_sources(reg, {0}, {})
+    fr = P.default_registry()
+    ctx = P.RankContext(vol, dom, reg, fr, fr.limits)
+    scene = P.SceneState(camera=P.Camera((20.0, 17.0, -9.0), (4.0, 4.0, 4.0), image_size=(32, 24)),
+                         settings=P.RenderSettings(active_set=(0,), early_termination_alpha=1.0))
+    with pytest.raises(P.GuardContractError):   # ... but trilinear needs i0 + 1 == size
+        P.render_local(ctx, scene)
+
+
+def test_value_range_bit_exact():
+    import paper_1611_09048_b200 as P
+    from oracle import isaac_oracle as O
+    torch = _torch()
+    rng = np.random.default_rng(5)
+    for dim, chain in ((1, ""), (1, "mul(-2) | add(0.25)"), (3, "length"), (3, "mul(1,2,3) | sum"),
+                       (4, "add(0.5) | length | mul(3)")):
+        arr = rng.standard_normal((14, 11, 19, dim) if dim > 1 else (14, 11, 19)).astype(np.float32)
+        arr[3, 4, 5] = np.nan if dim == 1 else arr[3, 4, 5]
+        dom = P.LocalDomain((0, 0, 0), (17, 9, 12), 1)
+        h = P.array_backed_handle(P.SourceDescriptor("v", dim, has_guard=True), torch.from_numpy(arr).cuda(), 1)
+        ch = P.parse_chain(chain, P.default_registry(), input_dim=dim)
+        lo, hi = P.value_range(h, dom, ch)
+        want = O.value_range(arr, 1, O.parse_steps(chain, dim))
+        assert np.float32(lo) == want[0] and np.float32(hi) == want[1], chain
+
+
+def test_kernel_nan_pow_chain_is_transparent():
+    import paper_1611_09048_b200 as P
+    torch = _torch()
+    n = 8
+    vol = P.GlobalVolume((n, n, n))
+    dom = vol.local_domain(0, 1)
+    reg = P.SourceRegistry(dom)
+    reg.register_handle(P.array_backed_handle(P.SourceDescriptor("f", 1, has_guard=True),
+                                              torch.full((n + 2,) * 3, -2.0, device="cuda"), 1))
+    P.update_sources(reg, {0}, {})
+    fr = P.default_registry()
+    ctx = P.RankContext(vol, dom, reg, fr, fr.limits)
+    scene = P.SceneState(camera=P.Camera((4.0, 4.0, -20.0), (4.0, 4.0, 4.0), image_size=(16, 16)),
+                         chain_texts={0: "pow(0.5)"},
+                         tf_points={0: [(0.0, 1.0, 1.0, 1.0, 1.0), (1.0, 1.0, 1.0, 1.0, 1.0)]},
+                         settings=P.RenderSettings(active_set=(0,), early_termination_alpha=1.0))
+    assert float(P.render_local(ctx, scene).pixels.abs().sum()) == 0.0
+
+
+def test_missing_device_op_raises_chain_error():
+    import paper_1611_09048_b200 as P
+    from product_build import product_ctx, product_scene
+    c = cases.case("c1")
+    ctx = product_ctx(c, (1, 1, 1), 0)
+    ctx.functor_registry.register_functor(P.FunctorDescriptor("half", False, lambda d: d),
+                                          {d: (lambda v, k: v / 2) for d in range(1, 5)})
+    scene = product_scene(c)
+    scene = P.SceneState(camera=scene.camera, tf_points=scene.tf_points, value_ranges=scene.value_ranges,
+                         chain_texts={0: "half"}, settings=scene.settings)
+    with pytest.raises(P.ChainError):
+        P.render_local(ctx, scene)
+    ctx.functor_registry.register_functor(P.FunctorDescriptor("sqrt", False, lambda d: d),
+                                          {d: (lambda v, k: np.sqrt(v)) for d in range(1, 5)})
+    scene = P.SceneState(camera=scene.camera, tf_points=scene.tf_points, value_ranges=scene.value_ranges,
+                         chain_texts={0: "sqrt"}, settings=scene.settings)
+    assert float(P.render_local(ctx, scene).pixels[..., 3].sum()) > 0
