@@ -39,57 +39,33 @@ def test_peer_memory_swap_sequential_launch(name):
             assert np.abs(out - gold["result"]).max() <= TOL
         R = len(imgs)
         image_bytes = h * w * 16
-        for ep in grp.endpoints:
-            assert ep.sent_bytes <= 3 * 2 * image_bytes and ep.received_bytes <= 3 * 2 * image_bytes
+        if R & (R - 1) == 0:   # binary swap balance bound (test_compositing.py:193-214), per epoch
+            for ep in grp.endpoints:
+                assert ep.sent_bytes <= 3 * 2 * image_bytes and ep.received_bytes <= 3 * 2 * image_bytes
     finally:
         grp.close()
 
 
-@pytest.mark.parametrize("ranks", [2, 4, 8, 3])
+@pytest.mark.parametrize("ranks", [2, 4, 8, 3, 6])
 def test_peer_memory_swap_concurrent_ranks(ranks):
     """Every rank on its own host thread + stream, all kernels live at once and
     order themselves through the flag protocol (the multi-GPU execution model,
-    here with all ranks sharing one device)."""
-    import torch
-    import paper_1611_09048_b200 as P
-    from oracle import isaac_oracle as O
-    rng = np.random.default_rng(ranks)
-    h, w = 37, 29
-    host = []
-    for _ in range(ranks):
-        a = rng.uniform(0, 1, (h, w, 1))
-        host.append(np.concatenate([rng.uniform(0, 1, (h, w, 3)) * a, a], axis=2))
-    order = [int(v) for v in rng.permutation(ranks)]
-    want = O.composite_in_order(host, order)
-    grp = P.LocalNvlinkGroup(ranks, h * w)
-    results = [None] * ranks
-    errors = []
-
-    def body(r):
-        try:
-            s = torch.cuda.Stream()
-            with torch.cuda.stream(s):
-                ep = grp.endpoints[r]
-                ep.n_ctas = 2
-                ep.timeout_s = 10.0
-                img = torch.from_numpy(host[r].astype(np.float32)).cuda()
-                for _ in range(2):
-                    out = P.binary_swap(ep, img, order)
-                results[r] = None if out is None else out.cpu().numpy()
-        except Exception as exc:  # noqa: BLE001
-            errors.append(exc)
-
-    try:
-        threads = [threading.Thread(target=body, args=(r,)) for r in range(ranks)]
-        for t in threads:
-            t.start()
-        for t in threads:
-            t.join(60)
-        assert not errors, errors
-        assert np.abs(results[0] - want).max() <= TOL
-        assert all(r is None for r in results[1:])
-    finally:
-        grp.close()
+    here with all ranks sharing one device), over 3 epochs.  Runs in a child
+    process with CUDA_DEVICE_MAX_CONNECTIONS=32 so the ranks' streams do not
+    alias onto one hardware queue (a single-GPU artefact)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    helper = os.path.join(os.path.dirname(os.path.abspath(__file__)), "helpers", "concurrent_swap.py")
+    env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="32")
+    out = subprocess.run([sys.executable, helper, str(ranks), "3"], env=env, capture_output=True, text=True,
+                         timeout=240)
+    assert out.returncode == 0, out.stderr[-2000:]
+    res = json.loads(out.stdout.strip().splitlines()[-1])
+    assert not res["errors"], res["errors"]
+    assert res["err"] is not None and res["err"] <= TOL
+    assert res["others_none"]
 
 
 @pytest.mark.parametrize("name", ["swap2", "swap8", "direct3", "direct6"])
