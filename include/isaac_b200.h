@@ -150,9 +150,11 @@ typedef struct {
                                 counted here (-> GuardContractError); optional */
   unsigned long long* out_station_total; /* device u64: sum of stations marched
                                 (LocalImage.stations, raycast.py:46); optional */
+  uint32_t* work_counter;    /* device u32 scratch for the persistent tile
+                                scheduler; optional (null = static grid) */
 } isc_render_args;
-/* isc_render_local zeroes *error_word and *out_station_total (stream-ordered)
- * before the march, so callers never need a separate fill. */
+/* isc_render_local zeroes *error_word, *out_station_total and *work_counter
+ * (stream-ordered) before the march, so callers never need a separate fill. */
 
 /* ---- library ------------------------------------------------------------ */
 ISC_API int isc_abi_version(void);

@@ -92,6 +92,7 @@ class RenderArgs(C.Structure):
         ("out_hit", C.c_void_p),
         ("error_word", C.c_void_p),
         ("out_station_total", C.c_void_p),
+        ("work_counter", C.c_void_p),
     ]
 
 

@@ -10,6 +10,8 @@
 // transfer-function LUTs of all active sources live in shared memory.
 #include <math_constants.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "raysetup.cuh"
 #include "sample.cuh"
@@ -223,6 +225,159 @@ __global__ void __launch_bounds__(kThreads) march_kernel(const __grid_constant__
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fast path: one active float32 scalar source in volume mode (the C1/C2/C4/C5
+// workloads).  Persistent warps pull 8x4-pixel tiles from an atomic counter
+// (dynamic load balance: ray lengths vary per tile), tiles ordered as 8x8
+// Morton blocks inside row-major super-tiles so concurrently marching warps
+// sit on neighbouring rays and share L1/L2 lines.  Element offsets are 32-bit
+// (the host checks the field fits), the guard contract is checked once on the
+// base cell, and two stations are issued per iteration so each warp keeps 16
+// independent gathers in flight.
+struct FastField {
+  const float* __restrict__ f;
+  int sx, sy, sz;        // element strides
+  int lo[3];             // brick offset - guard (global cell of array index 0)
+  int hi[3];             // largest legal base index (guarded) / size-1 (clamped)
+  int g;
+};
+
+template <bool INTERP, bool GUARDED>
+__device__ __forceinline__ float fast_sample(const FastField& F, const double p[3], uint32_t* err) {
+  int ix = __double2int_rd(p[0]), iy = __double2int_rd(p[1]), iz = __double2int_rd(p[2]);
+  if constexpr (!INTERP) {
+    // nearest: clamp the local cell into the brick (fields.py:240-242)
+    const int x = min(max(ix - F.lo[0] - F.g, 0), F.hi[0]) + F.g;
+    const int y = min(max(iy - F.lo[1] - F.g, 0), F.hi[1]) + F.g;
+    const int z = min(max(iz - F.lo[2] - F.g, 0), F.hi[2]) + F.g;
+    return __ldg(F.f + (z * F.sz + y * F.sy + x * F.sx));
+  } else {
+    const float fx = (float)dsub(p[0], (double)ix), fy = (float)dsub(p[1], (double)iy),
+                fz = (float)dsub(p[2], (double)iz);
+    int x0, y0, z0, dx, dy, dz;
+    if constexpr (GUARDED) {
+      x0 = ix - F.lo[0];
+      y0 = iy - F.lo[1];
+      z0 = iz - F.lo[2];
+      if ((unsigned)x0 > (unsigned)F.hi[0] || (unsigned)y0 > (unsigned)F.hi[1] || (unsigned)z0 > (unsigned)F.hi[2]) {
+        if (err) atomicAdd(err, 1u);
+        x0 = min(max(x0, 0), F.hi[0]);
+        y0 = min(max(y0, 0), F.hi[1]);
+        z0 = min(max(z0, 0), F.hi[2]);
+      }
+      dx = F.sx;
+      dy = F.sy;
+      dz = F.sz;
+    } else {
+      // clamp each corner index into the brick (fields.py:240-242)
+      const int lx = ix - F.lo[0] - F.g, ly = iy - F.lo[1] - F.g, lz = iz - F.lo[2] - F.g;
+      x0 = min(max(lx, 0), F.hi[0]);
+      y0 = min(max(ly, 0), F.hi[1]);
+      z0 = min(max(lz, 0), F.hi[2]);
+      dx = (min(max(lx + 1, 0), F.hi[0]) - x0) * F.sx;
+      dy = (min(max(ly + 1, 0), F.hi[1]) - y0) * F.sy;
+      dz = (min(max(lz + 1, 0), F.hi[2]) - z0) * F.sz;
+      x0 += F.g;
+      y0 += F.g;
+      z0 += F.g;
+    }
+    const float* b = F.f + (z0 * F.sz + y0 * F.sy + x0 * F.sx);
+    const float v000 = __ldg(b), v100 = __ldg(b + dx), v010 = __ldg(b + dy), v110 = __ldg(b + dy + dx);
+    const float* c = b + dz;
+    const float v001 = __ldg(c), v101 = __ldg(c + dx), v011 = __ldg(c + dy), v111 = __ldg(c + dy + dx);
+    const float a0 = fmaf(fx, v100 - v000, v000), a1 = fmaf(fx, v110 - v010, v010);
+    const float a2 = fmaf(fx, v101 - v001, v001), a3 = fmaf(fx, v111 - v011, v011);
+    const float b0 = fmaf(fy, a1 - a0, a0), b1 = fmaf(fy, a3 - a2, a2);
+    return fmaf(fz, b1 - b0, b0);
+  }
+}
+
+__device__ __forceinline__ int morton3(int w, int shift) {
+  return ((w >> shift) & 1) | (((w >> (shift + 2)) & 1) << 1) | (((w >> (shift + 4)) & 1) << 2);
+}
+
+template <bool INTERP, bool GUARDED>
+__global__ void __launch_bounds__(kThreads) march_fast_kernel(const __grid_constant__ isc_render_args a,
+                                                              const FastField F, int tiles_x, int tiles_y,
+                                                              int super_x, int n_codes) {
+  __shared__ float4 lut_s[ISC_LUT_ENTRIES];
+  for (int i = threadIdx.x; i < ISC_LUT_ENTRIES; i += blockDim.x)
+    lut_s[i] = reinterpret_cast<const float4*>(a.src[0].lut)[i];
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31;
+  const isc_source& s = a.src[0];
+  const float lo = s.range_lo, inv = 1.0f / (s.range_hi - s.range_lo);
+  const bool gate_alpha = a.alpha_stop < 1.0;
+  const double* o = a.camera.origin;
+  const double step = a.step;
+  uint32_t* err = a.error_word;
+  unsigned long long warp_stations = 0;
+
+  for (;;) {
+    int t = 0;
+    if (lane == 0) t = (int)atomicAdd(a.work_counter, 1u);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t >= n_codes) break;
+    const int sblk = t >> 6, w = t & 63;
+    const int tx = (sblk % super_x) * 8 + morton3(w, 0);
+    const int ty = (sblk / super_x) * 8 + morton3(w, 1);
+    if (tx >= tiles_x || ty >= tiles_y) continue;
+    const int px = tx * 8 + (lane & 7), py = ty * 4 + (lane >> 3);
+    if (px >= a.camera.width || py >= a.camera.height) continue;
+    const long long pix = (long long)py * a.camera.width + px;
+
+    Ray r;
+    setup_ray(a, px, py, r);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t stations = 0;
+    if (r.hit) {
+      long long k = r.k_lo;
+      if (!gate_alpha) {
+        for (; k + 1 < r.k_hi; k += 2) {  // two independent stations in flight
+          double p0[3], p1[3];
+          station_pos(o, r.d, dmul((double)k, step), p0);
+          station_pos(o, r.d, dmul((double)(k + 1), step), p1);
+          const float v0 = fast_sample<INTERP, GUARDED>(F, p0, err);
+          const float v1 = fast_sample<INTERP, GUARDED>(F, p1, err);
+          const float s0 = s.n_steps ? run_chain(s, &((float[4]){v0, 0.f, 0.f, 0.f})[0], 1) : v0;
+          const float s1 = s.n_steps ? run_chain(s, &((float[4]){v1, 0.f, 0.f, 0.f})[0], 1) : v1;
+          acc = over4(acc, premultiply(classify(lut_s, lo, inv, s0)));
+          acc = over4(acc, premultiply(classify(lut_s, lo, inv, s1)));
+        }
+        stations = (uint32_t)(r.k_hi - r.k_lo);
+      }
+      for (; k < r.k_hi; ++k) {
+        double p0[3];
+        station_pos(o, r.d, dmul((double)k, step), p0);
+        const float v0 = fast_sample<INTERP, GUARDED>(F, p0, err);
+        float vv[4] = {v0, 0.f, 0.f, 0.f};
+        const float s0 = s.n_steps ? run_chain(s, vv, 1) : v0;
+        acc = over4(acc, premultiply(classify(lut_s, lo, inv, s0)));
+        if (gate_alpha) {
+          ++stations;
+          if ((double)acc.w >= a.alpha_stop) break;
+        }
+      }
+    }
+    reinterpret_cast<float4*>(a.out_rgba)[pix] = acc;
+    warp_stations += stations;
+    if (a.out_stations) a.out_stations[pix] = stations;
+    if (a.out_hit) a.out_hit[pix] = r.hit ? 1 : 0;
+    if (a.out_t) {
+      a.out_t[2 * pix] = r.t_in;
+      a.out_t[2 * pix + 1] = r.t_out;
+    }
+    if (a.out_krange)
+      reinterpret_cast<int4*>(a.out_krange)[pix] = make_int4((int)r.k_lo, (int)r.k_hi, (int)r.kg_lo, (int)r.kg_hi);
+  }
+  if (a.out_station_total) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) warp_stations += __shfl_xor_sync(0xffffffffu, warp_stations, off);
+    if (lane == 0 && warp_stations) atomicAdd(a.out_station_total, warp_stations);
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) ray_setup_kernel(const __grid_constant__ isc_render_args a) {
   int px, py;
   tile_pixel(px, py);
@@ -275,12 +430,67 @@ static int validate(const isc_render_args* a, bool need_rgba) {
 
 using namespace isc;
 
+static bool fast_eligible(const isc_render_args* a, FastField& F) {
+  if (a->n_sources != 1 || !a->work_counter) return false;
+  const isc_source& s = a->src[0];
+  if (s.feature_dim != 1 || s.mode != ISC_VOLUME || s.dtype != ISC_F32) return false;
+  const int g = a->guard_width;
+  long long ext[3];
+  for (int i = 0; i < 3; ++i) ext[i] = a->brick_size[i] + 2LL * g;
+  // every index the kernel forms must fit in int32
+  long long maxoff = 0;
+  for (int i = 0; i < 3; ++i) {
+    if (s.stride[i] < 0 || s.stride[i] > INT32_MAX) return false;
+    maxoff += (ext[2 - i] - 1) * s.stride[i];
+  }
+  if (maxoff + s.stride[0] + s.stride[1] + s.stride[2] >= INT32_MAX) return false;
+  F.f = reinterpret_cast<const float*>(s.data);
+  F.sz = (int)s.stride[0];
+  F.sy = (int)s.stride[1];
+  F.sx = (int)s.stride[2];
+  F.g = g;
+  const bool guarded = s.has_guard && a->interpolation;
+  for (int i = 0; i < 3; ++i) {
+    F.lo[i] = a->brick_offset[i] - g;
+    F.hi[i] = guarded ? a->brick_size[i] + 2 * g - 2 : a->brick_size[i] - 1;
+  }
+  return true;
+}
+
+template <bool INTERP, bool GUARDED>
+static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_t st) {
+  const int tiles_x = (a->camera.width + 7) / 8, tiles_y = (a->camera.height + 3) / 4;
+  const int super_x = (tiles_x + 7) / 8, super_y = (tiles_y + 7) / 8;
+  const int n_codes = super_x * super_y * 64;
+  int dev = 0, sms = 148, per_sm = 1;
+  ISC_CUDA_CHECK(cudaGetDevice(&dev));
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_fast_kernel<INTERP, GUARDED>, kThreads, 0);
+  const int total_warps = (n_codes + 0);
+  int grid = sms * (per_sm > 0 ? per_sm : 1);
+  const int need = (total_warps + (kThreads / 32) - 1) / (kThreads / 32);
+  if (grid > need) grid = need > 0 ? need : 1;
+  march_fast_kernel<INTERP, GUARDED><<<grid, kThreads, 0, st>>>(*a, F, tiles_x, tiles_y, super_x, n_codes);
+  ISC_CUDA_CHECK(cudaGetLastError());
+  return ISC_OK;
+}
+
 extern "C" int isc_render_local(const isc_render_args* a, void* stream) {
   int st = validate(a, true);
   if (st != ISC_OK) return st;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (a->error_word) ISC_CUDA_CHECK(cudaMemsetAsync(a->error_word, 0, sizeof(uint32_t), s));
   if (a->out_station_total) ISC_CUDA_CHECK(cudaMemsetAsync(a->out_station_total, 0, sizeof(unsigned long long), s));
+  if (a->work_counter) ISC_CUDA_CHECK(cudaMemsetAsync(a->work_counter, 0, sizeof(uint32_t), s));
+  FastField F;
+  static const bool no_fast = getenv("ISC_DISABLE_FAST") != nullptr;
+  if (!no_fast && fast_eligible(a, F)) {
+    const bool interp = a->interpolation != 0;
+    const bool guarded = interp && a->src[0].has_guard;
+    if (interp && guarded) return launch_fast<true, true>(a, F, s);
+    if (interp) return launch_fast<true, false>(a, F, s);
+    return launch_fast<false, false>(a, F, s);
+  }
   dim3 grid((a->camera.width + kTile - 1) / kTile, (a->camera.height + kTile - 1) / kTile);
   const size_t smem = (size_t)a->n_sources * ISC_LUT_ENTRIES * sizeof(float4);
   const bool fast = a->n_sources == 1 && a->src[0].feature_dim == 1 && a->src[0].mode == ISC_VOLUME &&

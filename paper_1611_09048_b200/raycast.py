@@ -225,12 +225,13 @@ def render_local(rank_ctx, scene: SceneState, plans: Optional[Sequence[SourcePla
     per_px = keep_station_counts or station_recorder is not None
     counts = torch.empty(h * w, dtype=torch.int32, device=device) if per_px else None
     kr = torch.empty((h * w, 4), dtype=torch.int32, device=device) if (keep_krange or station_recorder) else None
-    stats = torch.empty(2, dtype=torch.int64, device=device)   # [station total, error word]; zeroed by the library
+    stats = torch.empty(3, dtype=torch.int64, device=device)   # [stations, error word, tile counter]; zeroed by the library
     args.out_rgba = ptr(out)
     args.out_stations = ptr(counts) if counts is not None else None
     args.out_krange = ptr(kr) if kr is not None else None
     args.out_station_total = ptr(stats)
     args.error_word = ptr(stats) + 8
+    args.work_counter = ptr(stats) + 16
     if events is not None:
         events[0].record(stream)
     _abi.check(_abi.lib().isc_render_local(C.byref(args), C.c_void_p(stream_handle(stream))), "render_local")
@@ -238,7 +239,7 @@ def render_local(rank_ctx, scene: SceneState, plans: Optional[Sequence[SourcePla
         events[1].record(stream)
 
     img = LocalImage(w, h, out)
-    img._error_word = stats[1:]
+    img._error_word = stats[1:2]
     img._stations = lambda: int(stats[0].item())
     taps = 8 if scene.settings.interpolation else 1
     for plan in plans:
