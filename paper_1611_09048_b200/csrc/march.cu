@@ -296,10 +296,25 @@ __device__ __forceinline__ int morton3(int w, int shift) {
   return ((w >> shift) & 1) | (((w >> (shift + 2)) & 1) << 1) | (((w >> (shift + 4)) & 1) << 2);
 }
 
-template <bool INTERP, bool GUARDED>
+// Exchange with lane ^ 16 only: the two lanes of a pair run identical trip
+// counts, other pairs of the warp may already have left the loop.
+__device__ __forceinline__ float4 shfl_pair(float4 v, unsigned mask) {
+  return make_float4(__shfl_xor_sync(mask, v.x, 16), __shfl_xor_sync(mask, v.y, 16),
+                     __shfl_xor_sync(mask, v.z, 16), __shfl_xor_sync(mask, v.w, 16));
+}
+
+// PAIRED: a warp is 16 rays (an 8x2 pixel tile) x 2 station parities; lanes l
+// and l+16 march the even / odd stations of the same ray half a cell apart, so
+// one gather request covers 32 samples within an ~8x2-pixel footprint (fewer
+// cache lines per request than an 8x4 tile).  Each station pair is merged in
+// order with one shuffle exchange: pair = s_even over s_odd, acc = acc over
+// pair -- the same over-sequence as the reference's per-station loop.
+// Used when early termination is off (alpha_stop >= 1).
+template <bool INTERP, bool GUARDED, bool PAIRED>
 __global__ void __launch_bounds__(kThreads) march_fast_kernel(const __grid_constant__ isc_render_args a,
                                                               const FastField F, int tiles_x, int tiles_y,
-                                                              int super_x, int n_codes) {
+                                                              int super_x, int n_codes, int row_order,
+                                                              int tw_log2) {
   __shared__ float4 lut_s[ISC_LUT_ENTRIES];
   for (int i = threadIdx.x; i < ISC_LUT_ENTRIES; i += blockDim.x)
     lut_s[i] = reinterpret_cast<const float4*>(a.src[0].lut)[i];
@@ -313,25 +328,64 @@ __global__ void __launch_bounds__(kThreads) march_fast_kernel(const __grid_const
   const double step = a.step;
   uint32_t* err = a.error_word;
   unsigned long long warp_stations = 0;
+  const int tw = 1 << tw_log2;
+  const int th = (PAIRED ? 16 : 32) >> tw_log2;
+  const int q = PAIRED ? (lane & 15) : lane;
+  const int parity = PAIRED ? (lane >> 4) : 0;
+  const unsigned pair_mask = (1u << lane) | (1u << (lane ^ 16));
 
   for (;;) {
     int t = 0;
     if (lane == 0) t = (int)atomicAdd(a.work_counter, 1u);
     t = __shfl_sync(0xffffffffu, t, 0);
     if (t >= n_codes) break;
-    const int sblk = t >> 6, w = t & 63;
-    const int tx = (sblk % super_x) * 8 + morton3(w, 0);
-    const int ty = (sblk / super_x) * 8 + morton3(w, 1);
+    int tx, ty;
+    if (row_order) {
+      tx = t % tiles_x;
+      ty = t / tiles_x;
+    } else {
+      const int sblk = t >> 6, w = t & 63;
+      tx = (sblk % super_x) * 8 + morton3(w, 0);
+      ty = (sblk / super_x) * 8 + morton3(w, 1);
+    }
     if (tx >= tiles_x || ty >= tiles_y) continue;
-    const int px = tx * 8 + (lane & 7), py = ty * 4 + (lane >> 3);
-    if (px >= a.camera.width || py >= a.camera.height) continue;
-    const long long pix = (long long)py * a.camera.width + px;
+    const int px = tx * tw + (q & (tw - 1)), py = ty * th + (q >> tw_log2);
+    const bool in_img = px < a.camera.width && py < a.camera.height;
+    if (!PAIRED && !in_img) continue;
 
     Ray r;
-    setup_ray(a, px, py, r);
+    if (in_img) {
+      setup_ray(a, px, py, r);
+    } else {
+      r.hit = false;
+      r.k_lo = r.k_hi = 0;
+    }
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     uint32_t stations = 0;
-    if (r.hit) {
+    if constexpr (PAIRED) {
+      // both lanes of a pair run the same trip count (pair-synchronous shuffles)
+      const long long n = r.hit ? (r.k_hi - r.k_lo) : 0;
+      const long long pairs = (n + 1) >> 1;
+      for (long long j = 0; j < pairs; ++j) {
+        const long long k = r.k_lo + 2 * j + parity;
+        float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (k < r.k_hi) {
+          double p0[3];
+          station_pos(o, r.d, dmul((double)k, step), p0);
+          const float v0 = fast_sample<INTERP, GUARDED>(F, p0, err);
+          float vv[4] = {v0, 0.f, 0.f, 0.f};
+          const float s0 = s.n_steps ? run_chain(s, vv, 1) : v0;
+          c = premultiply(classify(lut_s, lo, inv, s0));
+        }
+        const float4 other = shfl_pair(c, pair_mask);
+        acc = over4(acc, parity ? over4(other, c) : over4(c, other));
+      }
+      stations = parity ? 0u : (uint32_t)n;
+      if (parity || !in_img) {
+        warp_stations += stations;
+        continue;
+      }
+    } else if (r.hit) {
       long long k = r.k_lo;
       if (!gate_alpha) {
         for (; k + 1 < r.k_hi; k += 2) {  // two independent stations in flight
@@ -340,8 +394,9 @@ __global__ void __launch_bounds__(kThreads) march_fast_kernel(const __grid_const
           station_pos(o, r.d, dmul((double)(k + 1), step), p1);
           const float v0 = fast_sample<INTERP, GUARDED>(F, p0, err);
           const float v1 = fast_sample<INTERP, GUARDED>(F, p1, err);
-          const float s0 = s.n_steps ? run_chain(s, &((float[4]){v0, 0.f, 0.f, 0.f})[0], 1) : v0;
-          const float s1 = s.n_steps ? run_chain(s, &((float[4]){v1, 0.f, 0.f, 0.f})[0], 1) : v1;
+          float w0[4] = {v0, 0.f, 0.f, 0.f}, w1[4] = {v1, 0.f, 0.f, 0.f};
+          const float s0 = s.n_steps ? run_chain(s, w0, 1) : v0;
+          const float s1 = s.n_steps ? run_chain(s, w1, 1) : v1;
           acc = over4(acc, premultiply(classify(lut_s, lo, inv, s0)));
           acc = over4(acc, premultiply(classify(lut_s, lo, inv, s1)));
         }
@@ -360,6 +415,7 @@ __global__ void __launch_bounds__(kThreads) march_fast_kernel(const __grid_const
         }
       }
     }
+    const long long pix = (long long)py * a.camera.width + px;
     reinterpret_cast<float4*>(a.out_rgba)[pix] = acc;
     warp_stations += stations;
     if (a.out_stations) a.out_stations[pix] = stations;
@@ -457,20 +513,24 @@ static bool fast_eligible(const isc_render_args* a, FastField& F) {
   return true;
 }
 
-template <bool INTERP, bool GUARDED>
+template <bool INTERP, bool GUARDED, bool PAIRED>
 static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_t st) {
-  const int tiles_x = (a->camera.width + 7) / 8, tiles_y = (a->camera.height + 3) / 4;
+  static const int tw_log2 = getenv("ISC_TILE_W") ? __builtin_ctz(atoi(getenv("ISC_TILE_W"))) : 3;
+  const int tw = 1 << tw_log2, th = (PAIRED ? 16 : 32) >> tw_log2;
+  const int tiles_x = (a->camera.width + tw - 1) / tw, tiles_y = (a->camera.height + th - 1) / th;
   const int super_x = (tiles_x + 7) / 8, super_y = (tiles_y + 7) / 8;
-  const int n_codes = super_x * super_y * 64;
+  static const bool row_order = getenv("ISC_TILE_ROWS") != nullptr;
+  const int n_codes = row_order ? tiles_x * tiles_y : super_x * super_y * 64;
   int dev = 0, sms = 148, per_sm = 1;
   ISC_CUDA_CHECK(cudaGetDevice(&dev));
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_fast_kernel<INTERP, GUARDED>, kThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_fast_kernel<INTERP, GUARDED, PAIRED>, kThreads, 0);
   const int total_warps = (n_codes + 0);
   int grid = sms * (per_sm > 0 ? per_sm : 1);
   const int need = (total_warps + (kThreads / 32) - 1) / (kThreads / 32);
   if (grid > need) grid = need > 0 ? need : 1;
-  march_fast_kernel<INTERP, GUARDED><<<grid, kThreads, 0, st>>>(*a, F, tiles_x, tiles_y, super_x, n_codes);
+  march_fast_kernel<INTERP, GUARDED, PAIRED><<<grid, kThreads, 0, st>>>(*a, F, tiles_x, tiles_y, super_x, n_codes, row_order ? 1 : 0,
+                                                                 tw_log2);
   ISC_CUDA_CHECK(cudaGetLastError());
   return ISC_OK;
 }
@@ -487,9 +547,11 @@ extern "C" int isc_render_local(const isc_render_args* a, void* stream) {
   if (!no_fast && fast_eligible(a, F)) {
     const bool interp = a->interpolation != 0;
     const bool guarded = interp && a->src[0].has_guard;
-    if (interp && guarded) return launch_fast<true, true>(a, F, s);
-    if (interp) return launch_fast<true, false>(a, F, s);
-    return launch_fast<false, false>(a, F, s);
+    static const bool no_pair = getenv("ISC_DISABLE_PAIRED") != nullptr;
+    const bool paired = !no_pair && a->alpha_stop >= 1.0;
+    if (interp && guarded) return paired ? launch_fast<true, true, true>(a, F, s) : launch_fast<true, true, false>(a, F, s);
+    if (interp) return paired ? launch_fast<true, false, true>(a, F, s) : launch_fast<true, false, false>(a, F, s);
+    return paired ? launch_fast<false, false, true>(a, F, s) : launch_fast<false, false, false>(a, F, s);
   }
   dim3 grid((a->camera.width + kTile - 1) / kTile, (a->camera.height + kTile - 1) / kTile);
   const size_t smem = (size_t)a->n_sources * ISC_LUT_ENTRIES * sizeof(float4);
