@@ -92,6 +92,7 @@ class DeviceOps:
         return self.torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float32)).to(self.device)
 
     def over(self, front, back):
+        front, back = front.contiguous(), back.contiguous()
         out = self.torch.empty_like(front)
         _abi.check(_abi.lib().isc_over(C.c_void_p(out.data_ptr()), C.c_void_p(front.data_ptr()),
                                        C.c_void_p(back.data_ptr()), front.shape[0], self._s()), "over")
@@ -202,7 +203,7 @@ def _swap_bytes(transport, flat, order, shape, ops):
             raise CompositeError(f"round mismatch: expected {r}, got {msg.round_index} from rank {partner}")
         if msg.span_offset != keep[0] or msg.span_length != keep[1] - keep[0]:
             raise CompositeError("partner sent an unexpected span")
-        kept = mine[keep[0] - span_lo:keep[1] - span_lo].contiguous()
+        kept = mine[keep[0] - span_lo:keep[1] - span_lo]
         theirs = ops.from_array(msg.payload)
         mine = ops.over(theirs, kept) if pv < v else ops.over(kept, theirs)
         span_lo = keep[0]

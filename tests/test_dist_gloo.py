@@ -1,0 +1,102 @@
+"""Multi-process (world size 2 and 4, gloo, CPU) coverage of the N>1 host
+path: TorchDistTransport bytes, broadcast / gather, and the binary-swap /
+direct-send message schedule of ``binary_swap`` over a byte transport.  The
+per-pixel ``over`` is injected (the oracle's) because kernels need a GPU; the
+GPU tests cover the same schedule with the CUDA ``over``."""
+
+import os
+import pickle
+import socket
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+class OracleOps:
+    """Host stand-in for compositing.DeviceOps (test only)."""
+
+    def as_flat(self, pixels):
+        return np.ascontiguousarray(pixels, dtype=np.float64).reshape(-1, 4)
+
+    def to_bytes(self, span):
+        return np.ascontiguousarray(span, dtype="<f4").tobytes()
+
+    def from_array(self, arr):
+        return np.asarray(arr, dtype=np.float64)
+
+    def over(self, front, back):
+        from oracle import isaac_oracle as O
+        return O.over(front, back)
+
+    def fold(self, flats, order):
+        from oracle import isaac_oracle as O
+        return O.composite_in_order(flats, order)
+
+    def empty(self, n):
+        return np.empty((n, 4))
+
+
+def _worker(rank, world, port, out_dir, images, order):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1611_09048_b200.compositing import _swap_bytes
+    from paper_1611_09048_b200.transport import TorchDistTransport
+    from test_dist_gloo import OracleOps
+    t = TorchDistTransport()
+    res = {}
+    # point to point in both directions + collectives
+    peer = (rank + 1) % world
+    t.send(peer, f"hello from {rank}".encode())
+    res["p2p"] = t.receive((rank - 1) % world).decode()
+    res["bcast"] = t.broadcast_from_root(b"scene-bytes" if rank == 0 else None)
+    res["gather"] = t.gather_to_root(str(rank).encode())
+    res["allgather"] = t.all_gather(bytes([rank]))
+    ops = OracleOps()
+    flat = ops.as_flat(images[rank])
+    out = _swap_bytes(t, flat, list(order), tuple(images[rank].shape), ops)
+    res["frame"] = None if out is None else np.asarray(out)
+    res["sent"], res["received"] = t.sent_bytes, t.received_bytes
+    t.flush()
+    dist.barrier()
+    dist.destroy_process_group()
+    with open(os.path.join(out_dir, f"r{rank}.pkl"), "wb") as fh:
+        pickle.dump(res, fh)
+
+
+@pytest.mark.parametrize("world", [2, 4, 3])
+def test_gloo_transport_and_swap_schedule(tmp_path, world):
+    import torch.multiprocessing as mp
+    from oracle import isaac_oracle as O
+    rng = np.random.default_rng(world)
+    images = []
+    for _ in range(world):
+        a = rng.uniform(0, 1, (9, 7, 1))
+        images.append(np.concatenate([rng.uniform(0, 1, (9, 7, 3)) * a, a], axis=2))
+    order = [int(v) for v in rng.permutation(world)]
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), images, order), nprocs=world, join=True)
+    res = [pickle.load(open(tmp_path / f"r{r}.pkl", "rb")) for r in range(world)]
+    for r in range(world):
+        assert res[r]["p2p"] == f"hello from {(r - 1) % world}"
+        assert res[r]["bcast"] == b"scene-bytes"
+        assert res[r]["allgather"] == [bytes([q]) for q in range(world)]
+    assert res[0]["gather"] == [str(q).encode() for q in range(world)]
+    want = O.composite_in_order(images, order)
+    assert np.abs(res[0]["frame"] - want).max() <= 1e-6   # float32 wire payload
+    assert all(res[r]["frame"] is None for r in range(1, world))
+    if world & (world - 1) == 0:
+        image_bytes = images[0][..., 0].size * 16
+        for r in range(world):   # balance bound (test_compositing.py:193-214), control bytes excluded
+            assert res[r]["sent"] <= 2 * image_bytes + 256
