@@ -269,7 +269,7 @@ def run_b200(args):
             "metric": METRIC, "value": round(fps, 3), "unit": "frames/s", "n_gpus": world, "steps": k,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"C4: {cfg['desc']}" if args.config == "c4" else cfg["desc"],
+            "config": {"workload": f"{args.config.upper()}: {cfg['desc']}",
                        "volume": [n, n, n], "image": [w, h], "decomposition": list(decomp),
                        "samples_per_frame": samples_frame, "field_bytes_per_gpu": field.numel() * 4,
                        "l2": "inputs larger than L2 (field >> 126 MB); no flush needed",
@@ -277,7 +277,7 @@ def run_b200(args):
             "gsamples_per_s": round(gsps, 3),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "march_kernel<FAST,INTERP>", "kernel_ms": round(kernel_ms_max, 4),
+                         "kernel": "isc::march_fast_kernel<INTERP=1,GUARDED=1,PAIRED=1>", "kernel_ms": round(kernel_ms_max, 4),
                          "algorithmic_bytes_per_launch": int(br.item() / world)},
             "e2e": e2e,
             "gpu_launches": k * (1 + (1 if world > 1 else 0)),
@@ -463,7 +463,7 @@ def run_reference(args):
     line = {"metric": METRIC, "value": round(fps, 6), "unit": "frames/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(1000.0 / fps, 1), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"C4: {cfg['desc']}", "volume": [n, n, n], "image": [w, h],
+            "config": {"workload": f"{args.config.upper()}: {cfg['desc']}", "volume": [n, n, n], "image": [w, h],
                        "decomposition": list(decomp), "samples_per_frame": samples_frame},
             "gsamples_per_s": round(sps / 1e9, 6),
             "cpu_baseline": {"value": round(fps, 6), "unit": "frames/s", "cores": cores, "kind": "port",
