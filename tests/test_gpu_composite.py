@@ -117,3 +117,23 @@ def test_swap_timeout_surfaces_as_transport_error():
             P.binary_swap(ep, torch.zeros((8, 8, 4), device="cuda"), [0, 1])   # rank 1 never arrives
     finally:
         grp.close()
+
+
+@pytest.mark.parametrize("name,world", [("swap2", 2), ("swap4", 4), ("direct3", 3)])
+def test_multi_process_ipc_swap(name, world):
+    """Process-per-rank with CUDA IPC arenas (torchrun, all ranks on one GPU)."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    helper = os.path.join(os.path.dirname(os.path.abspath(__file__)), "helpers", "mp_swap.py")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", helper, name, "3"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=400)
+    assert out.returncode == 0, out.stderr[-3000:]
+    res = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert res["max_err"] <= TOL
