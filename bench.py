@@ -38,7 +38,12 @@ CONFIGS = {
                                                 "linear TF, harness camera, step 0.5, bricks across N GPUs"),
     "c2": dict(n=512, image=(1920, 1080), clip=True, desc="512^3 float32, 1920x1080, trilinear + clip plane"),
     "c1": dict(n=64, image=(256, 256), desc="64^3 float32, 256x256, trilinear, linear TF"),
+    "c3": dict(n=512, image=(1920, 1080), multi=True,
+               desc="512^3 scalar (iso surface) + 512^3 float3 (chain length|mul(2)|add(0.1), volume), 1920x1080"),
+    "c5": dict(n=512, image=(3840, 2160), weak=True, orbit=True,
+               desc="512^3 float32 per GPU (weak scaling), 3840x2160, 26-direction camera orbit"),
 }
+ORBIT = [(i, j, k) for i in (-1, 0, 1) for j in (-1, 0, 1) for k in (-1, 0, 1) if (i, j, k) != (0, 0, 0)]
 BYTES_PER_SAMPLE = 32       # 8 trilinear corners x 4 B
 BYTES_PER_PIXEL_OUT = 16    # float32 RGBA written per pixel
 
@@ -89,18 +94,54 @@ def make_field_torch(n, domain, device, dtype=None):
     return out
 
 
-def build_scene(P, cfg):
-    n = cfg["n"]
+def make_vector_field_torch(n, domain, device):
+    """float3 field for C3: three phase-shifted copies of the scalar field."""
+    import torch
+    g = domain.guard_width
+    sx, sy, sz = domain.size
+    out = torch.empty((sz + 2 * g, sy + 2 * g, sx + 2 * g, 3), dtype=torch.float32, device=device)
+    base = make_field_torch(n, domain, device)
+    out[..., 0] = base - 1.0
+    out[..., 1] = 0.5 * base
+    out[..., 2] = base.flip(0) - 1.0
+    return out
+
+
+def build_scene(P, cfg, n=None):
+    n = n if n is not None else cfg["n"]
     pos, look = harness_camera(n)
     planes = ()
     if cfg.get("clip"):
         planes = (P.clip_plane((n / 2.0,) * 3, (0.3, -0.5, 0.81)),)
+    linear = [(0.0, 0.0, 0.0, 0.0, 0.0), (1.0, 1.0, 1.0, 1.0, 1.0)]
+    if cfg.get("multi"):
+        cool = [(0.0, 0.0, 0.0, 0.0, 0.0), (0.6, 0.1, 0.7, 0.4, 0.3), (1.0, 0.7, 1.0, 0.9, 0.8)]
+        return P.SceneState(camera=P.Camera(pos, look, image_size=cfg["image"]),
+                            tf_points={0: linear, 1: cool}, value_ranges={0: (-0.4, 2.4), 1: (0.0, 6.0)},
+                            chain_texts={0: "", 1: "length | mul(2) | add(0.1)"},
+                            settings=P.RenderSettings(active_set=(0, 1), modes={0: "iso"},
+                                                      iso_thresholds={0: 1.0}, interpolation=True,
+                                                      step_length=0.5, early_termination_alpha=1.0),
+                            clip_planes=planes)
     return P.SceneState(camera=P.Camera(pos, look, image_size=cfg["image"]),
-                        tf_points={0: [(0.0, 0.0, 0.0, 0.0, 0.0), (1.0, 1.0, 1.0, 1.0, 1.0)]},
+                        tf_points={0: linear},
                         value_ranges={0: (-0.4, 2.4)}, chain_texts={0: ""},
                         settings=P.RenderSettings(active_set=(0,), interpolation=True, step_length=0.5,
                                                   early_termination_alpha=1.0),
                         clip_planes=planes)
+
+
+def orbit_scene(P, scene, n, dvec):
+    """Camera on the 26-direction orbit {-1,0,1}^3 minus 0 at
+    radius 1752 * n / 512 about the centre."""
+    c = n / 2.0
+    norm = math.sqrt(sum(v * v for v in dvec))
+    r = 1752.0 * n / 1024.0
+    pos = tuple(c + r * v / norm for v in dvec)
+    up = (0.0, 1.0, 0.0) if dvec[0] or dvec[2] else (0.0, 0.0, 1.0)
+    cam = P.Camera(pos, (c, c, c), up=up, image_size=scene.camera.image_size)
+    return P.SceneState(camera=cam, tf_points=scene.tf_points, value_ranges=scene.value_ranges,
+                        chain_texts=scene.chain_texts, settings=scene.settings, clip_planes=scene.clip_planes)
 
 
 class ClockSampler:
@@ -165,26 +206,42 @@ def run_b200(args):
     import paper_1611_09048_b200 as P
 
     rank, world, local = dist_env()
+    if args.share_gpu:          # test mode: every rank on cuda:0 (ranks time-share one GPU)
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    red_dev = torch.device("cpu") if args.share_gpu else dev
     cfg = CONFIGS[args.config]
-    n = cfg["n"]
     w, h = cfg["image"]
     decomp = DECOMP[world]
-    volume = P.GlobalVolume((n, n, n), decomp)
+    size = tuple(cfg["n"] * decomp[a] for a in range(3)) if cfg.get("weak") else (cfg["n"],) * 3
+    n = size[0]
+    volume = P.GlobalVolume(size, decomp)
     domain = volume.local_domain(rank, 1)
     t0 = time.time()
     field = make_field_torch(n, domain, dev)
-    torch.cuda.synchronize()
-    log(f"[rank {rank}] field {tuple(field.shape)} ready in {time.time() - t0:.1f}s")
     reg = P.SourceRegistry(domain)
     reg.register_handle(P.array_backed_handle(P.SourceDescriptor("density", 1, has_guard=True), field, 1))
-    P.update_sources(reg, {0}, {})
+    active = {0}
+    if cfg.get("multi"):
+        vec = make_vector_field_torch(n, domain, dev)
+        reg.register_handle(P.array_backed_handle(P.SourceDescriptor("velocity", 3, has_guard=True), vec, 1))
+        active = {0, 1}
+    torch.cuda.synchronize()
+    log(f"[rank {rank}] field {tuple(field.shape)} ready in {time.time() - t0:.1f}s")
+    P.update_sources(reg, active, {})
     fr = P.default_registry()
-    scene = build_scene(P, cfg)
-    order = P.visibility_order(volume, scene.camera)
+    scene = build_scene(P, cfg, n)
+    scenes = [scene]
+    if cfg.get("orbit"):
+        scenes = [orbit_scene(P, scene, n, dvec) for dvec in ORBIT]
+    orders = [P.visibility_order(volume, sc.camera) for sc in scenes]
+    order = orders[0]
     if world > 1:
         host = P.TorchDistTransport()
         transport = P.NvlinkTransport(host, w * h)
@@ -193,12 +250,15 @@ def run_b200(args):
         transport = P.LocalFabric(1).endpoint(0)
         canvas = torch.empty((h, w, 4), dtype=torch.float32, device=dev)
     ctx = P.RankContext(volume, domain, reg, fr, fr.limits, transport)
-    plans = P.build_plans(reg, fr, fr.limits, scene)
+    plans = [P.build_plans(reg, fr, fr.limits, sc) for sc in scenes]
     stream = torch.cuda.current_stream()
+    counter = [0]
 
     def step(events=None):
-        img = P.render_local(ctx, scene, plans=plans, out=canvas, check_errors=False, events=events)
-        full = P.binary_swap(transport, img.pixels, order)
+        i = counter[0] % len(scenes)
+        counter[0] += 1
+        img = P.render_local(ctx, scenes[i], plans=plans[i], out=canvas, check_errors=False, events=events)
+        full = P.binary_swap(transport, img.pixels, orders[i])
         return img, full
 
     def barrier():
@@ -212,7 +272,17 @@ def run_b200(args):
         img, _ = step()
     img.check()
     stations = img.stations
-    st_t = torch.tensor([stations], dtype=torch.float64, device=dev)
+    if len(scenes) > 1:       # orbit: samples per frame averaged over the timed camera sequence
+        counter[0] = 0
+        tot = 0
+        for _ in range(args.steps):
+            im, _ = step()
+            tot += im.stations
+        stations = tot / args.steps
+        counter[0] = 0
+    n_active = len(active)
+    bytes_per_station = sum(BYTES_PER_SAMPLE * reg.descriptor(sid).feature_dim for sid in sorted(active))
+    st_t = torch.tensor([stations * n_active], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(st_t)
     samples_frame = int(st_t.item())
@@ -233,7 +303,7 @@ def run_b200(args):
     clk = clocks.stop()
     ms_total = start.elapsed_time(end)
     kernel_ms = sum(a.elapsed_time(b) for a, b in evs) / k
-    t = torch.tensor([ms_total, kernel_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([ms_total, kernel_ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total, kernel_ms_max = float(t[0]), float(t[1])
@@ -242,8 +312,8 @@ def run_b200(args):
     gsps = samples_frame * fps / 1e9
 
     # roofline of the dominant kernel (the march): algorithmic bytes per launch
-    bytes_rank = stations * BYTES_PER_SAMPLE + w * h * BYTES_PER_PIXEL_OUT
-    br = torch.tensor([float(bytes_rank)], dtype=torch.float64, device=dev)
+    bytes_rank = stations * bytes_per_station + w * h * BYTES_PER_PIXEL_OUT
+    br = torch.tensor([float(bytes_rank)], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(br)
     peak, peak_src = peak_hbm()
@@ -258,7 +328,7 @@ def run_b200(args):
     # e2e through the public API with host buffers: scene bytes in (JSON, as
     # broadcast by the reference runtime) -> LUT + launch block H2D, frame out
     # to pinned host memory (D2H) every step.
-    e2e = run_e2e(P, torch, dist, ctx, scene, transport, canvas, order, rank, world, dev, max(2, k // 2))
+    e2e = run_e2e(P, torch, dist, ctx, scenes[0], transport, canvas, order, rank, world, red_dev, max(2, k // 2))
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -268,13 +338,15 @@ def run_b200(args):
         line = {
             "metric": METRIC, "value": round(fps, 3), "unit": "frames/s", "n_gpus": world, "steps": k,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{args.config.upper()}: {cfg['desc']}",
-                       "volume": [n, n, n], "image": [w, h], "decomposition": list(decomp),
+            "scaling": "weak" if cfg.get("weak") else "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": {"workload": f"{args.config.upper()}: {cfg['desc']}",
+                       "volume": list(size), "image": [w, h], "decomposition": list(decomp),
                        "samples_per_frame": samples_frame, "field_bytes_per_gpu": field.numel() * 4,
                        "l2": "inputs larger than L2 (field >> 126 MB); no flush needed",
                        "parallelism": f"bricks{decomp[0]}x{decomp[1]}x{decomp[2]}"},
             "gsamples_per_s": round(gsps, 3),
+            "samples_note": ("samples = stations x active sources; iso rays stop at the hit" if cfg.get("multi")
+                             else "samples = stations (one active source)"),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
                          "kernel": "isc::march_fast_kernel<INTERP=1,GUARDED=1,PAIRED=1>", "kernel_ms": round(kernel_ms_max, 4),
@@ -484,6 +556,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-step-s", type=float, default=4.0)
+    ap.add_argument("--share-gpu", action="store_true", help="test only: all ranks on cuda:0")
     args = ap.parse_args()
     if args.warmup < 3:
         log("note: warmup < 3 requested; using 3")
