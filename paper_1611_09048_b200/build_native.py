@@ -18,8 +18,8 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libisaac_b200.so")
-SOURCES = ["abi.cu", "march.cu", "minmax.cu", "composite.cu"]
-HEADERS = ["common.cuh", "raysetup.cuh", "sample.cuh"]
+SOURCES = ["abi.cu", "march.cu", "march_multi.cu", "minmax.cu", "composite.cu"]
+HEADERS = ["common.cuh", "raysetup.cuh", "sample.cuh", "march_common.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

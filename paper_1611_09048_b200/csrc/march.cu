@@ -13,13 +13,13 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "march_common.cuh"
 #include "raysetup.cuh"
 #include "sample.cuh"
 
 namespace isc {
 
-constexpr int kTile = 16;
-constexpr int kThreads = kTile * kTile;
+bool launch_multi(const isc_render_args* a, cudaStream_t st, int* status);  // march_multi.cu
 
 __device__ __forceinline__ void tile_pixel(int& px, int& py) {
   const int t = threadIdx.x, w = t >> 5, l = t & 31;
@@ -234,75 +234,6 @@ __global__ void __launch_bounds__(kThreads) march_kernel(const __grid_constant__
 // (the host checks the field fits), the guard contract is checked once on the
 // base cell, and two stations are issued per iteration so each warp keeps 16
 // independent gathers in flight.
-struct FastField {
-  const float* __restrict__ f;
-  int sx, sy, sz;        // element strides
-  int lo[3];             // brick offset - guard (global cell of array index 0)
-  int hi[3];             // largest legal base index (guarded) / size-1 (clamped)
-  int g;
-};
-
-template <bool INTERP, bool GUARDED>
-__device__ __forceinline__ float fast_sample(const FastField& F, const double p[3], uint32_t* err) {
-  int ix = __double2int_rd(p[0]), iy = __double2int_rd(p[1]), iz = __double2int_rd(p[2]);
-  if constexpr (!INTERP) {
-    // nearest: clamp the local cell into the brick (fields.py:240-242)
-    const int x = min(max(ix - F.lo[0] - F.g, 0), F.hi[0]) + F.g;
-    const int y = min(max(iy - F.lo[1] - F.g, 0), F.hi[1]) + F.g;
-    const int z = min(max(iz - F.lo[2] - F.g, 0), F.hi[2]) + F.g;
-    return __ldg(F.f + (z * F.sz + y * F.sy + x * F.sx));
-  } else {
-    const float fx = (float)dsub(p[0], (double)ix), fy = (float)dsub(p[1], (double)iy),
-                fz = (float)dsub(p[2], (double)iz);
-    int x0, y0, z0, dx, dy, dz;
-    if constexpr (GUARDED) {
-      x0 = ix - F.lo[0];
-      y0 = iy - F.lo[1];
-      z0 = iz - F.lo[2];
-      if ((unsigned)x0 > (unsigned)F.hi[0] || (unsigned)y0 > (unsigned)F.hi[1] || (unsigned)z0 > (unsigned)F.hi[2]) {
-        if (err) atomicAdd(err, 1u);
-        x0 = min(max(x0, 0), F.hi[0]);
-        y0 = min(max(y0, 0), F.hi[1]);
-        z0 = min(max(z0, 0), F.hi[2]);
-      }
-      dx = F.sx;
-      dy = F.sy;
-      dz = F.sz;
-    } else {
-      // clamp each corner index into the brick (fields.py:240-242)
-      const int lx = ix - F.lo[0] - F.g, ly = iy - F.lo[1] - F.g, lz = iz - F.lo[2] - F.g;
-      x0 = min(max(lx, 0), F.hi[0]);
-      y0 = min(max(ly, 0), F.hi[1]);
-      z0 = min(max(lz, 0), F.hi[2]);
-      dx = (min(max(lx + 1, 0), F.hi[0]) - x0) * F.sx;
-      dy = (min(max(ly + 1, 0), F.hi[1]) - y0) * F.sy;
-      dz = (min(max(lz + 1, 0), F.hi[2]) - z0) * F.sz;
-      x0 += F.g;
-      y0 += F.g;
-      z0 += F.g;
-    }
-    const float* b = F.f + (z0 * F.sz + y0 * F.sy + x0 * F.sx);
-    const float v000 = __ldg(b), v100 = __ldg(b + dx), v010 = __ldg(b + dy), v110 = __ldg(b + dy + dx);
-    const float* c = b + dz;
-    const float v001 = __ldg(c), v101 = __ldg(c + dx), v011 = __ldg(c + dy), v111 = __ldg(c + dy + dx);
-    const float a0 = fmaf(fx, v100 - v000, v000), a1 = fmaf(fx, v110 - v010, v010);
-    const float a2 = fmaf(fx, v101 - v001, v001), a3 = fmaf(fx, v111 - v011, v011);
-    const float b0 = fmaf(fy, a1 - a0, a0), b1 = fmaf(fy, a3 - a2, a2);
-    return fmaf(fz, b1 - b0, b0);
-  }
-}
-
-__device__ __forceinline__ int morton3(int w, int shift) {
-  return ((w >> shift) & 1) | (((w >> (shift + 2)) & 1) << 1) | (((w >> (shift + 4)) & 1) << 2);
-}
-
-// Exchange with lane ^ 16 only: the two lanes of a pair run identical trip
-// counts, other pairs of the warp may already have left the loop.
-__device__ __forceinline__ float4 shfl_pair(float4 v, unsigned mask) {
-  return make_float4(__shfl_xor_sync(mask, v.x, 16), __shfl_xor_sync(mask, v.y, 16),
-                     __shfl_xor_sync(mask, v.z, 16), __shfl_xor_sync(mask, v.w, 16));
-}
-
 // PAIRED: a warp is 16 rays (an 8x2 pixel tile) x 2 station parities; lanes l
 // and l+16 march the even / odd stations of the same ray half a cell apart, so
 // one gather request covers 32 samples within an ~8x2-pixel footprint (fewer
@@ -553,6 +484,9 @@ extern "C" int isc_render_local(const isc_render_args* a, void* stream) {
     if (interp) return paired ? launch_fast<true, false, true>(a, F, s) : launch_fast<true, false, false>(a, F, s);
     return paired ? launch_fast<false, false, true>(a, F, s) : launch_fast<false, false, false>(a, F, s);
   }
+  static const bool no_multi = getenv("ISC_DISABLE_MULTI") != nullptr;
+  int mstatus = ISC_OK;
+  if (!no_multi && launch_multi(a, s, &mstatus)) return mstatus;
   dim3 grid((a->camera.width + kTile - 1) / kTile, (a->camera.height + kTile - 1) / kTile);
   const size_t smem = (size_t)a->n_sources * ISC_LUT_ENTRIES * sizeof(float4);
   const bool fast = a->n_sources == 1 && a->src[0].feature_dim == 1 && a->src[0].mode == ISC_VOLUME &&

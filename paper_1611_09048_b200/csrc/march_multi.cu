@@ -1,0 +1,350 @@
+// Multi-source march (C3: scalar iso surface + float3 volume with a functor
+// chain, and any 1-4 float32 sources): the per-station loop of
+// raycast.march_rays (raycast.py:336-380) with every active source sampled in
+// source-id order, iso detection (_iso_detect, raycast.py:384-468) and
+// gradient shading (raycast.py:210-242, 351-369).
+//
+// Versus the generic kernel (march.cu): persistent warps on the Morton tile
+// scheduler, the exact float64 cell / fraction computed ONCE per station and
+// shared by all sources (they share the brick, raycast.py:86), 32-bit element
+// offsets, float32 loads without per-load dtype dispatch, the source loop
+// unrolled at compile time (NS = 1..4) so per-source iso state lives in
+// registers.  Iso side-samples (entry pair, exit pair, 6 gradient taps) are
+// rare and go through one out-of-line point sampler.
+#include "march_common.cuh"
+#include "sample.cuh"
+
+namespace isc {
+
+struct MultiSrc {
+  const float* __restrict__ f;
+  int sx, sy, sz, sc;   // element strides: x, y, z, component
+  int dim;
+  int guarded;          // has_guard && interpolation
+  int hi[3];            // guarded: size + 2g - 2 ; clamped: size - 1
+};
+
+struct MultiField {
+  MultiSrc s[4];
+  int lo[3];            // brick offset - guard
+  int g;
+};
+
+// dim components of one source at the cell (ix, iy, iz) + fractions.
+template <bool INTERP>
+__device__ __forceinline__ void multi_sample(const MultiSrc& S, const MultiField& M, int ix, int iy, int iz,
+                                             float fx, float fy, float fz, float v[4], uint32_t* err) {
+  const int g = M.g;
+  if constexpr (!INTERP) {
+    const int x = min(max(ix - M.lo[0] - g, 0), S.hi[0]) + g;
+    const int y = min(max(iy - M.lo[1] - g, 0), S.hi[1]) + g;
+    const int z = min(max(iz - M.lo[2] - g, 0), S.hi[2]) + g;
+    const float* b = S.f + (z * S.sz + y * S.sy + x * S.sx);
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (c < S.dim) v[c] = __ldg(b + c * S.sc);
+    return;
+  } else {
+    int x0, y0, z0, dx, dy, dz;
+    if (S.guarded) {
+      x0 = ix - M.lo[0];
+      y0 = iy - M.lo[1];
+      z0 = iz - M.lo[2];
+      if ((unsigned)x0 > (unsigned)S.hi[0] || (unsigned)y0 > (unsigned)S.hi[1] || (unsigned)z0 > (unsigned)S.hi[2]) {
+        if (err) atomicAdd(err, 1u);
+        x0 = min(max(x0, 0), S.hi[0]);
+        y0 = min(max(y0, 0), S.hi[1]);
+        z0 = min(max(z0, 0), S.hi[2]);
+      }
+      dx = S.sx;
+      dy = S.sy;
+      dz = S.sz;
+    } else {
+      const int lx = ix - M.lo[0] - g, ly = iy - M.lo[1] - g, lz = iz - M.lo[2] - g;
+      x0 = min(max(lx, 0), S.hi[0]);
+      y0 = min(max(ly, 0), S.hi[1]);
+      z0 = min(max(lz, 0), S.hi[2]);
+      dx = (min(max(lx + 1, 0), S.hi[0]) - x0) * S.sx;
+      dy = (min(max(ly + 1, 0), S.hi[1]) - y0) * S.sy;
+      dz = (min(max(lz + 1, 0), S.hi[2]) - z0) * S.sz;
+      x0 += g;
+      y0 += g;
+      z0 += g;
+    }
+    const float* b = S.f + (z0 * S.sz + y0 * S.sy + x0 * S.sx);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (c >= S.dim) break;
+      const float* p = b + c * S.sc;
+      const float v000 = __ldg(p), v100 = __ldg(p + dx), v010 = __ldg(p + dy), v110 = __ldg(p + dy + dx);
+      const float* q = p + dz;
+      const float v001 = __ldg(q), v101 = __ldg(q + dx), v011 = __ldg(q + dy), v111 = __ldg(q + dy + dx);
+      const float a0 = fmaf(fx, v100 - v000, v000), a1 = fmaf(fx, v110 - v010, v010);
+      const float a2 = fmaf(fx, v101 - v001, v001), a3 = fmaf(fx, v111 - v011, v011);
+      const float b0 = fmaf(fy, a1 - a0, a0), b1 = fmaf(fy, a3 - a2, a2);
+      v[c] = fmaf(fz, b1 - b0, b0);
+    }
+  }
+}
+
+__device__ __forceinline__ void cell_of(const double p[3], int& ix, int& iy, int& iz, float& fx, float& fy,
+                                        float& fz) {
+  ix = __double2int_rd(p[0]);
+  iy = __double2int_rd(p[1]);
+  iz = __double2int_rd(p[2]);
+  fx = (float)dsub(p[0], (double)ix);
+  fy = (float)dsub(p[1], (double)iy);
+  fz = (float)dsub(p[2], (double)iz);
+}
+
+// Chained scalar of one source at an arbitrary global position (iso extras).
+template <bool INTERP>
+__device__ __noinline__ float point_scalar(const MultiSrc& S, const MultiField& M, const isc_source& src,
+                                           const double p[3], uint32_t* err) {
+  int ix, iy, iz;
+  float fx, fy, fz;
+  cell_of(p, ix, iy, iz, fx, fy, fz);
+  float v[4] = {0.f, 0.f, 0.f, 0.f};
+  multi_sample<INTERP>(S, M, ix, iy, iz, fx, fy, fz, v, err);
+  return run_chain(src, v, S.dim);
+}
+
+__device__ __forceinline__ bool reach(const double off[3], const double size[3], int g, const double p[3]) {
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const double lo = dsub(off[i], (double)g);
+    const double hi = dsub(dadd(dadd(off[i], size[i]), (double)g), 1.0);
+    ok &= (p[i] >= lo) && (p[i] < hi);
+  }
+  return ok;
+}
+
+template <bool INTERP>
+__device__ __noinline__ float3 multi_normal(const MultiSrc& S, const MultiField& M, const isc_source& src,
+                                            const double off[3], const int size[3], const double p[3],
+                                            const double d[3], uint32_t* err) {
+  const int g = S.guarded ? M.g : 0;
+  float grad[3];
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    const double lo = dsub(off[ax], (double)g);
+    const double hi = dsub(dsub(dadd(dadd(lo, (double)size[ax]), (double)(2 * g)), 1.0), 1e-9);
+    double pp[3] = {p[0], p[1], p[2]}, pm[3] = {p[0], p[1], p[2]};
+    pp[ax] = dmin(dmax(dadd(p[ax], 1.0), lo), hi);
+    pm[ax] = dmin(dmax(dsub(p[ax], 1.0), lo), hi);
+    double span = dsub(pp[ax], pm[ax]);
+    if (span == 0.0) span = 1.0;
+    const float sp = point_scalar<INTERP>(S, M, src, pp, err);
+    const float sm = point_scalar<INTERP>(S, M, src, pm, err);
+    grad[ax] = (float)((double)(sp - sm) / span);
+  }
+  const float mag = sqrtf((grad[0] * grad[0] + grad[1] * grad[1]) + grad[2] * grad[2]);
+  if (mag < 1e-12f) {
+    const double dm = sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]);
+    return make_float3((float)(-d[0] / dm), (float)(-d[1] / dm), (float)(-d[2] / dm));
+  }
+  return make_float3(grad[0] / mag, grad[1] / mag, grad[2] / mag);
+}
+
+template <int NS, bool INTERP>
+__global__ void __launch_bounds__(kThreads) march_multi_kernel(const __grid_constant__ isc_render_args a,
+                                                               const __grid_constant__ MultiField M, int tiles_x,
+                                                               int tiles_y, int super_x, int n_codes) {
+  __shared__ float4 lut_s[NS * ISC_LUT_ENTRIES];
+  for (int i = threadIdx.x; i < NS * ISC_LUT_ENTRIES; i += blockDim.x)
+    lut_s[i] = reinterpret_cast<const float4*>(a.src[i >> 8].lut)[i & (ISC_LUT_ENTRIES - 1)];
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31;
+  const bool gate_alpha = a.alpha_stop < 1.0;
+  const double* o = a.camera.origin;
+  const double step = a.step;
+  uint32_t* err = a.error_word;
+  double off[3], bsz[3], vb[3];
+  int isz[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    off[i] = (double)a.brick_offset[i];
+    bsz[i] = (double)a.brick_size[i];
+    isz[i] = a.brick_size[i];
+    vb[i] = ddiv((double)a.volume_size[i], (double)a.decomposition[i]);  // raycast.py:283-285
+  }
+  float inv[NS];
+#pragma unroll
+  for (int si = 0; si < NS; ++si) inv[si] = 1.0f / (a.src[si].range_hi - a.src[si].range_lo);
+  unsigned long long warp_stations = 0;
+
+  for (;;) {
+    int t = 0;
+    if (lane == 0) t = (int)atomicAdd(a.work_counter, 1u);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t >= n_codes) break;
+    const int sblk = t >> 6, w = t & 63;
+    const int tx = (sblk % super_x) * 8 + morton3(w, 0);
+    const int ty = (sblk / super_x) * 8 + morton3(w, 1);
+    if (tx >= tiles_x || ty >= tiles_y) continue;
+    const int px = tx * 8 + (lane & 7), py = ty * 4 + (lane >> 3);
+    if (px >= a.camera.width || py >= a.camera.height) continue;
+
+    Ray r;
+    setup_ray(a, px, py, r);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t stations = 0;
+    if (r.hit) {
+      float prev[NS];
+#pragma unroll
+      for (int si = 0; si < NS; ++si) prev[si] = CUDART_NAN_F;
+      for (long long k = r.k_lo; k < r.k_hi; ++k) {
+        ++stations;
+        double p[3];
+        station_pos(o, r.d, dmul((double)k, step), p);
+        int ix, iy, iz;
+        float fx, fy, fz;
+        cell_of(p, ix, iy, iz, fx, fy, fz);
+        float4 st = make_float4(0.f, 0.f, 0.f, 0.f);
+        bool stop = false;
+#pragma unroll
+        for (int si = 0; si < NS; ++si) {
+          const isc_source& s = a.src[si];
+          const MultiSrc& S = M.s[si];
+          float v[4] = {0.f, 0.f, 0.f, 0.f};
+          multi_sample<INTERP>(S, M, ix, iy, iz, fx, fy, fz, v, err);
+          const float cur = s.n_steps ? run_chain(s, v, S.dim) : v[0];
+          const float4* lut = lut_s + si * ISC_LUT_ENTRIES;
+          if (s.mode != ISC_ISO) {
+            st = over4(st, premultiply(classify(lut, s.range_lo, inv[si], cur)));
+            continue;
+          }
+          // ---- iso: raycast.py:384-468 ----
+          const float thr = s.iso_threshold;
+          const bool exact = S.guarded != 0;
+          float before = prev[si];
+          if (k == r.k_lo && k - 1 >= r.kg_lo) {  // entry pair: sample k-1 through the guard
+            double pq[3];
+            station_pos(o, r.d, dmul((double)(k - 1), step), pq);
+            before = (!exact || reach(off, bsz, M.g, pq)) ? point_scalar<INTERP>(S, M, s, pq, err) : CUDART_NAN_F;
+          }
+          const float sa = before - thr, sb = cur - thr;
+          bool hit = isfinite(sa) && ((sa < 0.f) != (sb < 0.f));
+          double tau = 0.0, back = 0.0;
+          if (hit) {
+            const float den = sa - sb;
+            tau = den != 0.f ? (double)(sa / den) : 1.0;
+            back = -1.0;
+          }
+          if (exact && !hit && k == r.k_hi - 1 && k + 1 < r.kg_hi) {  // exit pair, checked forward
+            double pn[3], noff[3];
+            station_pos(o, r.d, dmul((double)(k + 1), step), pn);
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+              double c = floor(ddiv(pn[i], vb[i]));
+              c = dmin(dmax(c, 0.0), (double)(a.decomposition[i] - 1));
+              noff[i] = dmul(c, vb[i]);
+            }
+            if (reach(off, bsz, M.g, pn) && !reach(noff, vb, M.g, p)) {
+              const float sn = point_scalar<INTERP>(S, M, s, pn, err) - thr;
+              if ((sb < 0.f) != (sn < 0.f)) {
+                const float den = sb - sn;
+                tau = den != 0.f ? (double)(sb / den) : 1.0;
+                back = 0.0;
+                hit = true;
+              }
+            }
+          }
+          prev[si] = cur;
+          if (hit) {
+            double hp[3];
+            const double tt = dmul(dadd(tau, back), step);
+#pragma unroll
+            for (int i = 0; i < 3; ++i) hp[i] = dadd(p[i], dmul(tt, r.d[i]));
+            const float3 n = multi_normal<INTERP>(S, M, s, off, isz, hp, r.d, err);
+            const float shade = fabsf(n.x * (float)r.d[0] + n.y * (float)r.d[1] + n.z * (float)r.d[2]);
+            const float4 base = classify(lut, s.range_lo, inv[si], thr);
+            st = over4(st, make_float4(base.x * shade, base.y * shade, base.z * shade, 1.0f));
+            stop = true;
+          }
+        }
+        acc = over4(acc, st);
+        if (stop || (gate_alpha && (double)acc.w >= a.alpha_stop)) break;
+      }
+    }
+    const long long pix = (long long)py * a.camera.width + px;
+    reinterpret_cast<float4*>(a.out_rgba)[pix] = acc;
+    warp_stations += stations;
+    if (a.out_stations) a.out_stations[pix] = stations;
+    if (a.out_hit) a.out_hit[pix] = r.hit ? 1 : 0;
+    if (a.out_t) {
+      a.out_t[2 * pix] = r.t_in;
+      a.out_t[2 * pix + 1] = r.t_out;
+    }
+    if (a.out_krange)
+      reinterpret_cast<int4*>(a.out_krange)[pix] = make_int4((int)r.k_lo, (int)r.k_hi, (int)r.kg_lo, (int)r.kg_hi);
+  }
+  if (a.out_station_total) {
+#pragma unroll
+    for (int off2 = 16; off2 > 0; off2 >>= 1) warp_stations += __shfl_xor_sync(0xffffffffu, warp_stations, off2);
+    if (lane == 0 && warp_stations) atomicAdd(a.out_station_total, warp_stations);
+  }
+}
+
+template <int NS, bool INTERP>
+static int launch_multi_t(const isc_render_args* a, const MultiField& M, cudaStream_t st) {
+  const int tiles_x = (a->camera.width + 7) / 8, tiles_y = (a->camera.height + 3) / 4;
+  const int super_x = (tiles_x + 7) / 8, super_y = (tiles_y + 7) / 8;
+  const int n_codes = super_x * super_y * 64;
+  int dev = 0, sms = 148, per_sm = 1;
+  ISC_CUDA_CHECK(cudaGetDevice(&dev));
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_multi_kernel<NS, INTERP>, kThreads, 0);
+  int grid = sms * (per_sm > 0 ? per_sm : 1);
+  const int need = (n_codes + (kThreads / 32) - 1) / (kThreads / 32);
+  if (grid > need) grid = need > 0 ? need : 1;
+  march_multi_kernel<NS, INTERP><<<grid, kThreads, 0, st>>>(*a, M, tiles_x, tiles_y, super_x, n_codes);
+  ISC_CUDA_CHECK(cudaGetLastError());
+  return ISC_OK;
+}
+
+// Returns true (and the launch status in *status) when the multi kernel
+// handles this render: 1..4 float32 sources, 32-bit offsets, work counter.
+bool launch_multi(const isc_render_args* a, cudaStream_t st, int* status) {
+  const int ns = a->n_sources;
+  if (ns < 1 || ns > 4 || !a->work_counter) return false;
+  MultiField M;
+  const int g = a->guard_width;
+  for (int i = 0; i < 3; ++i) M.lo[i] = a->brick_offset[i] - g;
+  M.g = g;
+  const bool interp = a->interpolation != 0;
+  for (int si = 0; si < ns; ++si) {
+    const isc_source& s = a->src[si];
+    if (s.dtype != ISC_F32) return false;
+    long long maxoff = (s.feature_dim - 1) * s.stride[3];
+    for (int i = 0; i < 3; ++i) {
+      if (s.stride[i] < 0 || s.stride[i] > INT32_MAX || s.stride[3] < 0 || s.stride[3] > INT32_MAX) return false;
+      maxoff += (a->brick_size[2 - i] + 2LL * g - 1) * s.stride[i];
+    }
+    if (maxoff >= INT32_MAX) return false;
+    MultiSrc& S = M.s[si];
+    S.f = reinterpret_cast<const float*>(s.data);
+    S.sz = (int)s.stride[0];
+    S.sy = (int)s.stride[1];
+    S.sx = (int)s.stride[2];
+    S.sc = (int)s.stride[3];
+    S.dim = s.feature_dim;
+    S.guarded = (s.has_guard && interp) ? 1 : 0;
+    for (int i = 0; i < 3; ++i) S.hi[i] = S.guarded ? a->brick_size[i] + 2 * g - 2 : a->brick_size[i] - 1;
+  }
+  switch (ns * 2 + (interp ? 1 : 0)) {
+    case 2: *status = launch_multi_t<1, false>(a, M, st); break;
+    case 3: *status = launch_multi_t<1, true>(a, M, st); break;
+    case 4: *status = launch_multi_t<2, false>(a, M, st); break;
+    case 5: *status = launch_multi_t<2, true>(a, M, st); break;
+    case 6: *status = launch_multi_t<3, false>(a, M, st); break;
+    case 7: *status = launch_multi_t<3, true>(a, M, st); break;
+    case 8: *status = launch_multi_t<4, false>(a, M, st); break;
+    default: *status = launch_multi_t<4, true>(a, M, st); break;
+  }
+  return true;
+}
+
+}  // namespace isc
