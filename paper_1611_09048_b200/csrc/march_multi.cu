@@ -147,8 +147,8 @@ __device__ __noinline__ float3 multi_normal(const MultiSrc& S, const MultiField&
   return make_float3(grad[0] / mag, grad[1] / mag, grad[2] / mag);
 }
 
-template <int NS, bool INTERP>
-__global__ void __launch_bounds__(kThreads) march_multi_kernel(const __grid_constant__ isc_render_args a,
+template <int NS, bool INTERP, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) march_multi_kernel(const __grid_constant__ isc_render_args a,
                                                                const __grid_constant__ MultiField M, int tiles_x,
                                                                int tiles_y, int super_x, int n_codes) {
   __shared__ float4 lut_s[NS * ISC_LUT_ENTRIES];
@@ -288,21 +288,27 @@ __global__ void __launch_bounds__(kThreads) march_multi_kernel(const __grid_cons
   }
 }
 
-template <int NS, bool INTERP>
-static int launch_multi_t(const isc_render_args* a, const MultiField& M, cudaStream_t st) {
+template <int NS, bool INTERP, int MINB>
+static int launch_multi_m(const isc_render_args* a, const MultiField& M, cudaStream_t st) {
   const int tiles_x = (a->camera.width + 7) / 8, tiles_y = (a->camera.height + 3) / 4;
   const int super_x = (tiles_x + 7) / 8, super_y = (tiles_y + 7) / 8;
   const int n_codes = super_x * super_y * 64;
   int dev = 0, sms = 148, per_sm = 1;
   ISC_CUDA_CHECK(cudaGetDevice(&dev));
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_multi_kernel<NS, INTERP>, kThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_multi_kernel<NS, INTERP, MINB>, kThreads, 0);
   int grid = sms * (per_sm > 0 ? per_sm : 1);
   const int need = (n_codes + (kThreads / 32) - 1) / (kThreads / 32);
   if (grid > need) grid = need > 0 ? need : 1;
-  march_multi_kernel<NS, INTERP><<<grid, kThreads, 0, st>>>(*a, M, tiles_x, tiles_y, super_x, n_codes);
+  march_multi_kernel<NS, INTERP, MINB><<<grid, kThreads, 0, st>>>(*a, M, tiles_x, tiles_y, super_x, n_codes);
   ISC_CUDA_CHECK(cudaGetLastError());
   return ISC_OK;
+}
+
+template <int NS, bool INTERP>
+static int launch_multi_t(const isc_render_args* a, const MultiField& M, cudaStream_t st) {
+  // 2 CTAs/SM (<= 128 registers): measured best; 3-4 CTAs spill (C3: 192.6 / 184.7 vs 198.7 fps)
+  return launch_multi_m<NS, INTERP, 2>(a, M, st);
 }
 
 // Returns true (and the launch status in *status) when the multi kernel
