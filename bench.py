@@ -330,6 +330,8 @@ def run_b200(args):
     # to pinned host memory (D2H) every step.
     e2e = run_e2e(P, torch, dist, ctx, scenes[0], transport, canvas, order, rank, world, red_dev, max(2, k // 2))
 
+    norm = time_normalisation(P, torch, reg, domain, peak)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(field, domain, volume, scene, samples_frame, budget_s=args.cpu_budget)
@@ -352,6 +354,7 @@ def run_b200(args):
                          "kernel": "isc::march_fast_kernel<INTERP=1,GUARDED=1,PAIRED=1>", "kernel_ms": round(kernel_ms_max, 4),
                          "algorithmic_bytes_per_launch": int(br.item() / world)},
             "e2e": e2e,
+            "normalisation": norm,
             "gpu_launches": k * (1 + (1 if world > 1 else 0)),
             "clocks": clk,
         }
@@ -361,6 +364,29 @@ def run_b200(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def time_normalisation(P, torch, reg, domain, peak, reps=10):
+    """Per-source normalisation pass (isc_value_range: min/max of the chained
+    scalar over the brick interior, warp-shuffle reduction) on source 0."""
+    from paper_1611_09048_b200.normalize import value_range_device
+    h = reg.render_handle(0)
+    out = torch.empty(4, dtype=torch.float32, device="cuda")
+    for _ in range(2):
+        value_range_device(h, domain, out=out)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        value_range_device(h, domain, out=out)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / reps
+    nbytes = domain.size[0] * domain.size[1] * domain.size[2] * 4 * h.descriptor.feature_dim
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    return {"kernel": "isc::minmax_kernel<DIM=1,F32>", "ms": round(ms, 4), "bytes": nbytes,
+            "achieved_GBps": round(gbs, 1), "frac_of_hbm_peak": round(gbs / peak, 4),
+            "range": [float(v) for v in out[:2].tolist()], "note": "L2-cold: field >> L2"}
 
 
 def run_e2e(P, torch, dist, ctx, scene, transport, canvas, order, rank, world, red_dev, steps):

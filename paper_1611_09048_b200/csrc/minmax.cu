@@ -3,8 +3,8 @@
 // function for this (value ranges are scene state, scene.py:188,
 // runtime.py:154-157); it feeds the auto value range of a transfer function.
 //
-// Streaming reduction: each warp walks whole x-rows (coalesced loads, 4 rows
-// in flight per warp for memory-level parallelism), reduces with warp
+// Streaming reduction: each warp walks whole x-rows (coalesced loads, 4
+// loads per lane in flight for memory-level parallelism), reduces with warp
 // shuffles, then one shared-memory pass per CTA and one ordered-integer
 // atomicMin/atomicMax per CTA.  min/max are exact, so the result is
 // bit-identical to the oracle regardless of reduction order.
@@ -26,7 +26,7 @@ __global__ void minmax_init(unsigned int* keys) {
   keys[1] = 0u;           // running max key
 }
 
-template <int DIM>
+template <int DIM, bool F32>
 __global__ void __launch_bounds__(256) minmax_kernel(const __grid_constant__ isc_source s, int sx, int sy, int sz,
                                                       int g, unsigned int* keys) {
   const int lane = threadIdx.x & 31;
@@ -35,20 +35,35 @@ __global__ void __launch_bounds__(256) minmax_kernel(const __grid_constant__ isc
   const long long rows = (long long)sy * sz;
   float lo = CUDART_INF_F, hi = -CUDART_INF_F;
   bool any = false;
+  auto visit = [&](float r) {
+    if (r == r) {
+      lo = fminf(lo, r);
+      hi = fmaxf(hi, r);
+      any = true;
+    }
+  };
   for (long long row = warp; row < rows; row += nwarps) {
     const int y = (int)(row % sy), z = (int)(row / sy);
-    const long long base = (long long)(z + g) * s.stride[0] + (long long)(y + g) * s.stride[1];
-    for (int x = lane; x < sx; x += 32) {
-      const long long e = base + (long long)(x + g) * s.stride[2];
+    const long long base = (long long)(z + g) * s.stride[0] + (long long)(y + g) * s.stride[1] + (long long)g * s.stride[2];
+    // 4 independent loads per lane in flight (memory-level parallelism)
+    int x = lane;
+    for (; x + 96 < sx; x += 128) {
+      float v[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const long long e = base + (long long)(x + 32 * u) * s.stride[2];
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) v[u][c] = load_as<F32>(s, e + c * s.stride[3]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) visit(run_chain(s, v[u], DIM));
+    }
+    for (; x < sx; x += 32) {
+      const long long e = base + (long long)x * s.stride[2];
       float v[4];
 #pragma unroll
-      for (int c = 0; c < DIM; ++c) v[c] = load_elem(s, e + c * s.stride[3]);
-      const float r = run_chain(s, v, DIM);
-      if (r == r) {
-        lo = fminf(lo, r);
-        hi = fmaxf(hi, r);
-        any = true;
-      }
+      for (int c = 0; c < DIM; ++c) v[c] = load_as<F32>(s, e + c * s.stride[3]);
+      visit(run_chain(s, v, DIM));
     }
   }
 #pragma unroll
@@ -109,11 +124,21 @@ extern "C" int isc_value_range(const isc_source* src, const int32_t brick_size[3
   const long long want = (rows + 7) / 8;  // 8 warps per CTA, >= 1 row per warp
   const int grid = (int)(want < (long long)sms * 8 ? (want > 0 ? want : 1) : (long long)sms * 8);
   minmax_init<<<1, 1, 0, s>>>(keys);
-  switch (src->feature_dim) {
-    case 1: minmax_kernel<1><<<grid, 256, 0, s>>>(*src, brick_size[0], brick_size[1], brick_size[2], guard, keys); break;
-    case 2: minmax_kernel<2><<<grid, 256, 0, s>>>(*src, brick_size[0], brick_size[1], brick_size[2], guard, keys); break;
-    case 3: minmax_kernel<3><<<grid, 256, 0, s>>>(*src, brick_size[0], brick_size[1], brick_size[2], guard, keys); break;
-    default: minmax_kernel<4><<<grid, 256, 0, s>>>(*src, brick_size[0], brick_size[1], brick_size[2], guard, keys); break;
+  const int bx = brick_size[0], by = brick_size[1], bz = brick_size[2];
+  if (src->dtype == ISC_F32) {
+    switch (src->feature_dim) {
+      case 1: minmax_kernel<1, true><<<grid, 256, 0, s>>>(*src, bx, by, bz, guard, keys); break;
+      case 2: minmax_kernel<2, true><<<grid, 256, 0, s>>>(*src, bx, by, bz, guard, keys); break;
+      case 3: minmax_kernel<3, true><<<grid, 256, 0, s>>>(*src, bx, by, bz, guard, keys); break;
+      default: minmax_kernel<4, true><<<grid, 256, 0, s>>>(*src, bx, by, bz, guard, keys); break;
+    }
+  } else {
+    switch (src->feature_dim) {
+      case 1: minmax_kernel<1, false><<<grid, 256, 0, s>>>(*src, bx, by, bz, guard, keys); break;
+      case 2: minmax_kernel<2, false><<<grid, 256, 0, s>>>(*src, bx, by, bz, guard, keys); break;
+      case 3: minmax_kernel<3, false><<<grid, 256, 0, s>>>(*src, bx, by, bz, guard, keys); break;
+      default: minmax_kernel<4, false><<<grid, 256, 0, s>>>(*src, bx, by, bz, guard, keys); break;
+    }
   }
   minmax_finish<<<1, 1, 0, s>>>(keys, out_minmax);
   ISC_CUDA_CHECK(cudaGetLastError());

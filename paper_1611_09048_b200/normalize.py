@@ -22,7 +22,7 @@ from .device import as_device_field, dtype_code, ptr, require_cuda, stream_handl
 from .errors import FieldError
 from .functors import FunctorChain, FunctorRegistry, default_registry, device_program, parse_chain
 
-__all__ = ["value_range", "auto_value_ranges"]
+__all__ = ["value_range", "value_range_device", "auto_value_ranges"]
 
 
 def _source_struct(array, guard_arr: int, guard_dom: int, feature_dim: int, chain: Optional[FunctorChain],
@@ -46,13 +46,9 @@ def _source_struct(array, guard_arr: int, guard_dom: int, feature_dim: int, chai
     return s
 
 
-def value_range(handle, domain, chain: Optional[FunctorChain] = None, *, group=None, stream=None):
-    """(min, max) of the chained scalar of ``handle`` over ``domain``'s interior.
-
-    With ``group`` (a torch.distributed process group, or True for WORLD) the
-    per-rank results are all-reduced (MIN / MAX) so every rank gets the global
-    range.  NaN samples are ignored; (nan, nan) if a brick has no value.
-    """
+def value_range_device(handle, domain, chain: Optional[FunctorChain] = None, *, out=None, stream=None):
+    """Asynchronous form: launches ``isc_value_range`` and returns the (4,)
+    float32 device tensor whose first two entries become (min, max)."""
     device = require_cuda()
     array, guard = handle.device_view(domain) if hasattr(handle, "device_view") else (handle, domain.guard_width)
     dim = handle.descriptor.feature_dim if hasattr(handle, "descriptor") else (1 if array.dim() == 3 else array.shape[3])
@@ -61,13 +57,21 @@ def value_range(handle, domain, chain: Optional[FunctorChain] = None, *, group=N
         raise FieldError(f"array shape {tuple(array.shape)} does not match domain size + 2*guard {need}")
     keep: list = []
     src = _source_struct(array, guard, 0, dim, chain, device, keep)
-    # Interior only: index with a zero halo from the interior origin.
-    st = list(src.stride)
-    src.data = ptr(keep[0]) + guard * (st[0] + st[1] + st[2]) * keep[0].element_size()
-    out = torch.empty(4, dtype=torch.float32, device=device)
+    out = out if out is not None else torch.empty(4, dtype=torch.float32, device=device)
     size = (C.c_int32 * 3)(*[int(v) for v in domain.size])
     _abi.check(_abi.lib().isc_value_range(C.byref(src), size, 0, C.c_void_p(out.data_ptr()),
                                           C.c_void_p(stream_handle(stream))), "value_range")
+    return out
+
+
+def value_range(handle, domain, chain: Optional[FunctorChain] = None, *, group=None, stream=None):
+    """(min, max) of the chained scalar of ``handle`` over ``domain``'s interior.
+
+    With ``group`` (a torch.distributed process group, or True for WORLD) the
+    per-rank results are all-reduced (MIN / MAX) so every rank gets the global
+    range.  NaN samples are ignored; (nan, nan) if a brick has no value.
+    """
+    out = value_range_device(handle, domain, chain, stream=stream)
     mm = out[:2].clone()
     if group is not None:
         import torch.distributed as dist
