@@ -216,3 +216,119 @@ def test_missing_device_op_raises_chain_error():
     scene = P.SceneState(camera=scene.camera, tf_points=scene.tf_points, value_ranges=scene.value_ranges,
                          chain_texts={0: "sqrt"}, settings=scene.settings)
     assert float(P.render_local(ctx, scene).pixels[..., 3].sum()) > 0
+
+
+def _single_source_scene(P, n, pos, look, chain="", tf=None, rng=(0.0, 1.0), active=(0,), extra=0):
+    tf = tf or [(0.0, 0.0, 0.1, 0.2, 0.0), (0.5, 0.9, 0.4, 0.1, 0.3), (1.0, 1.0, 1.0, 0.5, 0.8)]
+    ids = list(range(1 + extra))
+    return P.SceneState(camera=P.Camera(pos, look, image_size=(48, 32)),
+                        tf_points={i: tf for i in ids}, value_ranges={i: rng for i in ids},
+                        chain_texts={i: chain for i in ids},
+                        settings=P.RenderSettings(active_set=tuple(active), early_termination_alpha=1.0))
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float16", "bfloat16"])
+def test_generic_kernel_other_dtypes(dtype):
+    """Non-float32 fields take the generic kernel (any dtype, 64-bit offsets)."""
+    import paper_1611_09048_b200 as P
+    from oracle import isaac_oracle as O
+    torch = _torch()
+    n = 20
+    rng = np.random.default_rng(3)
+    host = rng.random((n + 2, n + 2, n + 2)).astype(np.float32)
+    t = torch.from_numpy(host).to(getattr(torch, dtype)).cuda()
+    vals = t.float().cpu().numpy()               # what the kernel actually reads
+    vol = P.GlobalVolume((n, n, n))
+    dom = vol.local_domain(0, 1)
+    reg = P.SourceRegistry(dom)
+    reg.register_handle(P.array_backed_handle(P.SourceDescriptor("f", 1, has_guard=True), t, 1))
+    P.update_sources(reg, {0}, {})
+    fr = P.default_registry()
+    ctx = P.RankContext(vol, dom, reg, fr, fr.limits)
+    pos, look = (31.0, 27.0, -22.0), (10.0, 10.0, 10.0)
+    scene = _single_source_scene(P, n, pos, look)
+    got = P.render_local(ctx, scene).pixels.cpu().numpy()
+    src = O.Source(array=vals.astype(np.float64), offset=(0, 0, 0), size=(n, n, n), guard=1,
+                   lut=O.lut_from_points(scene.tf_points[0]), value_range=(0.0, 1.0))
+    ref = O.render_brick({"position": pos, "look_at": look, "width": 48, "height": 32},
+                         O.Brick((0, 0, 0), (n, n, n), 1, (n, n, n)), [src])
+    assert np.abs(got - ref.rgba).max() <= RGBA_TOL
+
+
+def test_generic_kernel_many_sources():
+    """Six active sources (more than the multi kernel's 4) -> generic kernel."""
+    import paper_1611_09048_b200 as P
+    from oracle import isaac_oracle as O
+    torch = _torch()
+    n = 16
+    rng = np.random.default_rng(4)
+    arrays = [rng.random((n + 2, n + 2, n + 2)).astype(np.float32) * 0.4 for _ in range(6)]
+    vol = P.GlobalVolume((n, n, n))
+    dom = vol.local_domain(0, 1)
+    reg = P.SourceRegistry(dom)
+    for i, a in enumerate(arrays):
+        reg.register_handle(P.array_backed_handle(P.SourceDescriptor(f"s{i}", 1, has_guard=True),
+                                                  torch.from_numpy(a).cuda(), 1))
+    P.update_sources(reg, set(range(6)), {})
+    fr = P.default_registry()
+    ctx = P.RankContext(vol, dom, reg, fr, fr.limits)
+    pos, look = (25.0, 21.0, -17.0), (8.0, 8.0, 8.0)
+    scene = _single_source_scene(P, n, pos, look, chain="mul(1.5) | add(0.05)", active=range(6), extra=5)
+    got = P.render_local(ctx, scene).pixels.cpu().numpy()
+    srcs = [O.Source(array=a, offset=(0, 0, 0), size=(n, n, n), guard=1, steps=O.parse_steps("mul(1.5) | add(0.05)", 1),
+                     lut=O.lut_from_points(scene.tf_points[0]), value_range=(0.0, 1.0)) for a in arrays]
+    ref = O.render_brick({"position": pos, "look_at": look, "width": 48, "height": 32},
+                         O.Brick((0, 0, 0), (n, n, n), 1, (n, n, n)), srcs)
+    assert np.abs(got - ref.rgba).max() <= RGBA_TOL
+
+
+def test_zero_copy_strided_views():
+    """A brick that is a strided view into a larger simulation buffer (padded
+    rows, interleaved components) renders identically to a packed copy."""
+    import paper_1611_09048_b200 as P
+    torch = _torch()
+    n = 18
+    rng = np.random.default_rng(5)
+    big = torch.from_numpy(rng.random((n + 2, n + 9, n + 7, 2)).astype(np.float32)).cuda()
+    view = big[:, 3:n + 5, 1:n + 3, 1]               # (z, y, x) with non-unit x stride
+    assert not view.is_contiguous()
+    packed = view.contiguous()
+    vol = P.GlobalVolume((n, n, n))
+    dom = vol.local_domain(0, 1)
+    imgs = []
+    for arr in (view, packed):
+        reg = P.SourceRegistry(dom)
+        reg.register_handle(P.array_backed_handle(P.SourceDescriptor("f", 1, has_guard=True), arr, 1))
+        P.update_sources(reg, {0}, {})
+        fr = P.default_registry()
+        ctx = P.RankContext(vol, dom, reg, fr, fr.limits)
+        scene = _single_source_scene(P, n, (30.0, -9.0, 33.0), (9.0, 9.0, 9.0))
+        imgs.append(P.render_local(ctx, scene).pixels.cpu().numpy())
+    assert np.array_equal(imgs[0], imgs[1])
+
+
+def test_numpy_and_sampler_sources_are_staged():
+    """numpy arrays and Python samplers are materialised on the device per frame."""
+    import paper_1611_09048_b200 as P
+    torch = _torch()
+    n = 12
+    rng = np.random.default_rng(6)
+    arr = rng.random((n + 2, n + 2, n + 2)).astype(np.float32)
+    vol = P.GlobalVolume((n, n, n))
+    dom = vol.local_domain(0, 1)
+    scene = _single_source_scene(P, n, (20.0, 17.0, -14.0), (6.0, 6.0, 6.0))
+    out = []
+    for kind in ("torch", "numpy", "sampler"):
+        reg = P.SourceRegistry(dom)
+        if kind == "torch":
+            reg.register_handle(P.array_backed_handle(P.SourceDescriptor("f", 1, has_guard=True),
+                                                      torch.from_numpy(arr).cuda(), 1))
+        elif kind == "numpy":
+            reg.register_handle(P.array_backed_handle(P.SourceDescriptor("f", 1, has_guard=True), arr, 1))
+        else:
+            reg.register_source(P.SourceDescriptor("f", 1, has_guard=True), None,
+                                batch_sampler=lambda x, y, z: arr[z + 1, y + 1, x + 1])
+        P.update_sources(reg, {0}, {})
+        fr = P.default_registry()
+        out.append(P.render_local(P.RankContext(vol, dom, reg, fr, fr.limits), scene).pixels.cpu().numpy())
+    assert np.array_equal(out[0], out[1]) and np.array_equal(out[0], out[2])
