@@ -34,6 +34,7 @@
  *   isc_composite_fold <- compositing.composite_sequential compositing.py:66-77
  *                         and _direct_send           compositing.py:184-194
  *   isc_binary_swap    <- compositing.binary_swap   compositing.py:107-181
+ *   isc_to_rgba8       <- runtime.to_rgba8           runtime.py:66-67
  *   isc_arena_* / isc_ipc_* <- transport.Transport  transport.py:20-28
  *                         (the NVLink replacement of LocalFabric queues)
  */
@@ -219,6 +220,11 @@ ISC_API int isc_swap_status(unsigned long long* flags, void* stream, int32_t* ou
  * rank's image (peer loads) in visibility order into root_out; other ranks
  * publish readiness and wait until rank 0 has finished reading them. */
 ISC_API int isc_direct_send(const isc_swap_args* args, void* stream);
+
+/* ---- frame encode ---------------------------------------------------------- */
+/* out[i] = round_half_even(clip(rgba[i], 0, 1) * 255) per channel, uint8
+ * (H, W, 4) -- runtime.to_rgba8 (runtime.py:66-67). */
+ISC_API int isc_to_rgba8(const float* rgba, uint8_t* out, int64_t n_pixels, void* stream);
 
 /* ---- device memory shared between processes --------------------------- */
 ISC_API int isc_arena_alloc(size_t bytes, void** out_ptr);     /* cudaMalloc + zero */

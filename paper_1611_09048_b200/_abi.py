@@ -139,6 +139,7 @@ _SIGNATURES = {
     "isc_ipc_open": (C.c_int, [C.c_char * IPC_HANDLE_BYTES, C.POINTER(C.c_void_p)]),
     "isc_ipc_close": (C.c_int, [C.c_void_p]),
     "isc_enable_peer_access": (C.c_int, [C.c_int]),
+    "isc_to_rgba8": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
 }
 
 EXPORTED = tuple(_SIGNATURES)

@@ -1,0 +1,266 @@
+"""Per-frame pipeline around the hot path (the caller of render_local /
+binary_swap): scene broadcast -> update_sources ->
+render -> visibility order -> binary swap -> metadata merge -> background
+encode/send on rank 0.
+
+Mirrors ``insitu.runtime`` (runtime.py:36-388) minus steering (the gateway /
+steering control plane is out of scope; a root-side ``steer`` hook can be
+plugged in).  The B200 differences: the frame stays on the device until
+``to_rgba8`` quantises it there (``isc_to_rgba8``), so 8.3 MB instead of 33 MB
+per 1080p frame crosses PCIe, and that copy runs on a side stream while the
+next frame renders (FrameStreamer overlap, runtime.py:187-249).
+"""
+
+from __future__ import annotations
+
+import base64
+import ctypes as C
+import io
+import json
+import logging
+import threading
+import time
+from dataclasses import dataclass, field
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+from . import _abi
+from .compositing import binary_swap, visibility_order
+from .errors import ChainError
+from .fields import update_sources
+from .functors import parse_chain
+from .scene import SceneState
+
+log = logging.getLogger(__name__)
+
+RAW_RGBA8 = "raw-rgba8"
+PNG = "png"
+
+__all__ = ["RAW_RGBA8", "PNG", "FrameAborted", "to_rgba8", "encode_frame", "decode_frame", "merge_metadata",
+           "FrameStreamer", "FrameResult", "PipelineContext", "broadcast_scene", "frame_pipeline"]
+
+
+class FrameAborted(Exception):
+    def __init__(self, reason: str, controls: Optional[list] = None):
+        super().__init__(reason)
+        self.controls = controls or []
+
+
+def to_rgba8(image, stream=None):
+    """round(clip(rgba, 0, 1) * 255) as uint8 (runtime.py:66-67), on the device.
+    Accepts a CUDA float32 (H, W, 4) tensor (or anything torch.as_tensor takes)."""
+    import torch
+    from .device import require_cuda, stream_handle
+    dev = require_cuda()
+    t = torch.as_tensor(image)
+    t = t.to(device=dev, dtype=torch.float32).contiguous()
+    if t.shape[-1] != 4:
+        raise ValueError(f"expected (..., 4) RGBA, got {tuple(t.shape)}")
+    out = torch.empty(t.shape, dtype=torch.uint8, device=dev)
+    _abi.check(_abi.lib().isc_to_rgba8(C.c_void_p(t.data_ptr()), C.c_void_p(out.data_ptr()), t.numel() // 4,
+                                       C.c_void_p(stream_handle(stream))), "to_rgba8")
+    return out
+
+
+def _encode_bytes(data: np.ndarray, encoding: str) -> str:
+    if encoding == RAW_RGBA8:
+        raw = data.tobytes()
+    elif encoding == PNG:
+        from PIL import Image
+        buf = io.BytesIO()
+        Image.fromarray(data, mode="RGBA").save(buf, format="PNG")
+        raw = buf.getvalue()
+    else:
+        raise ValueError(f"unknown frame encoding {encoding!r}")
+    return base64.b64encode(raw).decode("ascii")
+
+
+def encode_frame(image, encoding: str = RAW_RGBA8, quality: Optional[int] = None) -> str:
+    """Quantise on the device, then base64 (raw) or PNG+base64 on the host (runtime.py:45-63)."""
+    return _encode_bytes(to_rgba8(image).cpu().numpy(), encoding)
+
+
+def decode_frame(data: str, width: int, height: int, encoding: str = RAW_RGBA8) -> np.ndarray:
+    raw = base64.b64decode(data)
+    if encoding == RAW_RGBA8:
+        return np.frombuffer(raw, dtype=np.uint8).reshape(height, width, 4)
+    if encoding == PNG:
+        from PIL import Image
+        return np.asarray(Image.open(io.BytesIO(raw)).convert("RGBA"))
+    raise ValueError(f"unknown frame encoding {encoding!r}")
+
+
+def merge_metadata(per_rank_docs: Sequence[dict]) -> dict:
+    """Rank-ordered merge; all-list keys concatenate, others keep the first (runtime.py:81-100)."""
+    seen: dict = {}
+    for doc in per_rank_docs:
+        for k, v in (doc or {}).items():
+            seen.setdefault(k, []).append(v)
+    return {k: ([x for v in vs for x in v] if len(vs) > 1 and all(isinstance(v, list) for v in vs) else vs[0])
+            for k, vs in seen.items()}
+
+
+class FrameStreamer:
+    """Root-side background encode + send, one frame in flight (runtime.py:187-249).
+
+    ``submit`` quantises the frame on the device, starts its D2H on a side
+    stream and returns; a worker thread waits for the copy, encodes and calls
+    ``sink(message)``.  ``wait_previous`` is the single per-frame rendezvous.
+    """
+
+    def __init__(self, sink: Callable[[dict], None], encoding: str = RAW_RGBA8):
+        import torch
+        self.sink = sink
+        self.encoding = encoding
+        self.timeline: list = []
+        self._thread: Optional[threading.Thread] = None
+        self._error: Optional[BaseException] = None
+        self._stream = torch.cuda.Stream()
+        self._host = None
+
+    def mark(self, event: str, step: int) -> None:
+        self.timeline.append((event, step, time.monotonic()))
+
+    def wait_previous(self) -> None:
+        if self._thread is not None:
+            self._thread.join()
+            self._thread = None
+        if self._error is not None:
+            err, self._error = self._error, None
+            raise RuntimeError(f"frame sink failed: {err}") from err
+
+    def submit(self, frame, step: int, metadata: dict, scene: SceneState) -> None:
+        import torch
+        self.wait_previous()
+        q = to_rgba8(frame)
+        ready = torch.cuda.Event()
+        ready.record()
+        if self._host is None or self._host.shape != q.shape:
+            self._host = torch.empty(q.shape, dtype=torch.uint8).pin_memory()
+        host = self._host
+        self._stream.wait_event(ready)
+        with torch.cuda.stream(self._stream):
+            host.copy_(q, non_blocking=True)
+            q.record_stream(self._stream)
+        done = torch.cuda.Event()
+        done.record(self._stream)
+        h, w = int(q.shape[0]), int(q.shape[1])
+
+        def work():
+            try:
+                self.mark("send_begin", step)
+                done.synchronize()
+                msg = {"type": "frame", "step": step, "width": w, "height": h, "encoding": self.encoding,
+                       "data": _encode_bytes(host.numpy(), self.encoding), "metadata": metadata,
+                       "scene_version": scene.version}
+                self.sink(msg)
+                self.mark("send_end", step)
+            except BaseException as exc:  # noqa: BLE001 -- surfaced at the rendezvous
+                self._error = exc
+
+        self._thread = threading.Thread(target=work, daemon=True)
+        self._thread.start()
+
+
+@dataclass
+class FrameResult:
+    step: int
+    image: object
+    metadata: dict
+    controls: list
+    render_seconds: float
+    composite_seconds: float
+    stations: int
+    aborted: bool = False
+
+
+@dataclass
+class PipelineContext:
+    """What one rank carries across frames (runtime.py:262-281, steering omitted)."""
+
+    transport: object
+    global_volume: object
+    domain: object
+    registry: object
+    functor_registry: object
+    limits: object
+    scene: SceneState
+    streamer: Optional[FrameStreamer] = None
+    metadata_hook: Optional[Callable[[int], dict]] = None
+    steer: Optional[Callable[[SceneState], tuple]] = None    # root: scene -> (scene, controls)
+    canvas: object = None
+
+    @property
+    def rank(self) -> int:
+        return self.transport.rank
+
+    @property
+    def is_root(self) -> bool:
+        return self.transport.rank == 0
+
+
+def broadcast_scene(ctx: PipelineContext, scene: Optional[SceneState] = None, controls: Sequence = ()):
+    """Root's scene (+ controls) to every rank as JSON bytes; a chain that no
+    longer parses aborts the frame everywhere and keeps the previous scene
+    (runtime.py:305-333)."""
+    if ctx.is_root:
+        env: dict = {"controls": list(controls)}
+        try:
+            for sid in scene.settings.active_set:
+                parse_chain(scene.chain_text(sid), ctx.functor_registry, ctx.limits,
+                            ctx.registry.descriptor(sid).feature_dim)
+            env["scene"] = scene.to_json()
+        except ChainError as exc:
+            env["abort"] = str(exc)
+            env["scene"] = ctx.scene.to_json()
+        payload = json.dumps(env, sort_keys=True).encode("utf-8")
+        ctx.transport.broadcast_from_root(payload)
+    else:
+        env = json.loads(ctx.transport.broadcast_from_root(None).decode("utf-8"))
+    ctx.scene = SceneState.from_json(env["scene"])
+    if "abort" in env:
+        raise FrameAborted(env["abort"], list(env.get("controls", ())))
+    return ctx.scene, list(env.get("controls", ()))
+
+
+def frame_pipeline(ctx: PipelineContext, frame_payload: dict) -> Optional[FrameResult]:
+    """One frame on this rank (runtime.py:336-388).  Rank 0 hands the frame to
+    the streamer and returns while it is encoded/sent in the background."""
+    import torch
+    from .raycast import render_local
+    step = int(frame_payload.get("step", 0))
+    scene, controls = ctx.scene, []
+    if ctx.is_root:
+        if ctx.streamer is not None:
+            ctx.streamer.wait_previous()
+        if ctx.steer is not None:
+            scene, controls = ctx.steer(ctx.scene)
+    try:
+        scene, controls = broadcast_scene(ctx, scene, controls)
+    except FrameAborted as abort:
+        return FrameResult(step, None, {}, abort.controls, 0.0, 0.0, 0, aborted=True)
+    update_sources(ctx.registry, scene.settings.active_set, frame_payload)
+    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    if ctx.is_root and ctx.streamer is not None:
+        ctx.streamer.mark("render_begin", step)
+    e0.record()
+    out = ctx.canvas if ctx.canvas is not None and tuple(ctx.canvas.shape[:2]) == scene.camera.image_size[::-1] \
+        else None
+    image = render_local(ctx, scene, out=out)
+    e1.record()
+    order = visibility_order(ctx.global_volume, scene.camera)
+    image.order_key = order.index(ctx.rank)
+    full = binary_swap(ctx.transport, image.pixels, order)
+    e2.record()
+    e2.synchronize()
+    render_s, comp_s = e0.elapsed_time(e1) / 1e3, e1.elapsed_time(e2) / 1e3
+    doc = dict(ctx.metadata_hook(step) if ctx.metadata_hook is not None else {})
+    doc.setdefault("render_ms", [render_s * 1000.0])
+    gathered = ctx.transport.gather_to_root(json.dumps(doc).encode("utf-8"))
+    metadata: dict = {}
+    if ctx.is_root:
+        metadata = merge_metadata([json.loads(d.decode("utf-8")) for d in gathered])
+        if ctx.streamer is not None:
+            ctx.streamer.submit(full, step, metadata, scene)
+    return FrameResult(step, full if ctx.is_root else None, metadata, controls, render_s, comp_s, image.stations)

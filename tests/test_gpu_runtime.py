@@ -1,0 +1,97 @@
+"""GPU tests of the per-frame caller: device to_rgba8 / encode, FrameStreamer
+overlap and frame_pipeline (runtime.py:45-388 restated)."""
+
+import base64
+import threading
+
+import numpy as np
+import pytest
+
+from case_build import full_fields
+from golden_io import cases, load
+
+pytestmark = pytest.mark.gpu
+
+
+def test_to_rgba8_bit_exact_vs_numpy():
+    import torch
+    from paper_1611_09048_b200.runtime import to_rgba8
+    rng = np.random.default_rng(0)
+    img = rng.uniform(-0.2, 1.2, (37, 53, 4)).astype(np.float32)
+    img[0, :8, 0] = np.array([0.5, 1.5, 2.5, 127.5, 254.5, 0.49999997, 0.50000006, 1.0], np.float32) / 255.0
+    want = (np.clip(img, 0.0, 1.0) * 255.0).round().astype(np.uint8)   # runtime.py:66-67 on the same f32
+    got = to_rgba8(torch.from_numpy(img).cuda()).cpu().numpy()
+    assert np.array_equal(got, want)
+
+
+def test_encode_decode_round_trip():
+    import torch
+    from paper_1611_09048_b200.runtime import PNG, RAW_RGBA8, decode_frame, encode_frame, to_rgba8
+    rng = np.random.default_rng(1)
+    img = torch.from_numpy(rng.random((20, 30, 4), dtype=np.float32)).cuda()
+    q = to_rgba8(img).cpu().numpy()
+    for enc in (RAW_RGBA8, PNG):
+        assert np.array_equal(decode_frame(encode_frame(img, enc), 30, 20, enc), q)
+    assert base64.b64decode(encode_frame(img)) == q.tobytes()
+
+
+def _pipeline_ctx(P, c, decomp, rank, transport, full, streamer=None):
+    from product_build import product_ctx, product_scene
+    from paper_1611_09048_b200.runtime import PipelineContext
+    rc = product_ctx(c, decomp, rank, full)
+    return PipelineContext(transport=transport, global_volume=rc.global_volume, domain=rc.domain,
+                           registry=rc.registry, functor_registry=rc.functor_registry, limits=rc.limits,
+                           scene=product_scene(c), streamer=streamer)
+
+
+def test_frame_pipeline_single_rank_with_streamer():
+    import paper_1611_09048_b200 as P
+    from paper_1611_09048_b200.runtime import FrameStreamer, decode_frame, frame_pipeline, to_rgba8
+    c = cases.case("multi")
+    gold = load("render_multi.npz")
+    full = full_fields(c)
+    sent = []
+    streamer = FrameStreamer(sent.append)
+    ctx = _pipeline_ctx(P, c, (1, 1, 1), 0, P.LocalFabric(1).endpoint(0), full, streamer)
+    results = [frame_pipeline(ctx, {"step": s}) for s in range(3)]
+    streamer.wait_previous()
+    assert [m["step"] for m in sent] == [0, 1, 2]
+    frame = results[-1].image
+    assert np.abs(frame.cpu().numpy() - gold["d111_composite"]).max() <= 1e-3
+    w, h = c["camera"]["image_size"]
+    assert np.array_equal(decode_frame(sent[-1]["data"], w, h), to_rgba8(frame).cpu().numpy())
+    ev = [e for e, _, _ in streamer.timeline]
+    assert ev.count("send_end") == 3 and results[-1].stations > 0 and results[-1].render_seconds > 0
+
+
+def test_frame_pipeline_two_ranks_byte_transport():
+    """Two ranks (threads, LocalFabric bytes + GPU over) through frame_pipeline:
+    rank 0's frame equals the reference's 2-brick composite."""
+    import torch
+    import paper_1611_09048_b200 as P
+    from paper_1611_09048_b200.runtime import frame_pipeline
+    c = cases.case("multi")
+    gold = load("render_multi.npz")
+    full = full_fields(c)
+    fabric = P.LocalFabric(2)
+    out = [None, None]
+    errs = []
+
+    def body(r):
+        try:
+            with torch.cuda.stream(torch.cuda.Stream()):
+                ctx = _pipeline_ctx(P, c, (2, 1, 1), r, fabric.endpoint(r), full)
+                res = frame_pipeline(ctx, {"step": 7})
+                out[r] = res
+        except Exception as exc:  # noqa: BLE001
+            errs.append(exc)
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(120)
+    assert not errs, errs
+    assert out[1].image is None and out[0].image is not None
+    assert np.abs(out[0].image.cpu().numpy() - gold["d211_composite"]).max() <= 1e-3
+    assert len(out[0].metadata["render_ms"]) == 2

@@ -263,3 +263,36 @@ def test_pack_render_args_on_host_tensors():
                          build_plans(bad, fr, fr.limits, P.SceneState(camera=scene.camera,
                                                                       settings=P.RenderSettings(active_set=(0,)))),
                          torch.device("cpu"), [])
+
+
+# ---- runtime host logic (runtime.py:81-100, 305-333) ------------------------
+
+def test_merge_metadata_rules():
+    from paper_1611_09048_b200.runtime import merge_metadata
+    assert merge_metadata([{"a": 1}, {"a": 2}]) == {"a": 1}
+    assert merge_metadata([{"v": [1]}, {"v": [2, 3]}]) == {"v": [1, 2, 3]}
+    assert len(merge_metadata([{f"k{i}": i} for i in range(12)])) == 12
+    doc = {"a": 1, "v": [1, 2], "o": {"x": 1}}
+    assert merge_metadata([doc]) == doc
+
+
+def test_broadcast_scene_aborts_on_bad_chain_everywhere():
+    from paper_1611_09048_b200.runtime import FrameAborted, PipelineContext, broadcast_scene
+    dom = P.LocalDomain((0, 0, 0), (4, 4, 4), 1)
+    good = P.SceneState(camera=P.Camera((10, 10, -10), (2, 2, 2), image_size=(8, 8)), chain_texts={0: "add(1)"},
+                        settings=P.RenderSettings(active_set=(0,)))
+    bad = good.bump(chain_texts={0: "nosuch"})
+
+    def body(t):
+        reg = P.SourceRegistry(dom)
+        reg.register_source(P.SourceDescriptor("f", 1), lambda i, j, k: P.field_vector(1.0))
+        fr = P.default_registry()
+        ctx = PipelineContext(t, None, dom, reg, fr, fr.limits, good)
+        ok = broadcast_scene(ctx, good if t.rank == 0 else None)[0]
+        try:
+            broadcast_scene(ctx, bad if t.rank == 0 else None)
+            return "no-abort"
+        except FrameAborted:
+            return (ok == good, ctx.scene == good)
+
+    assert P.run_ranks(3, body) == [(True, True)] * 3
