@@ -69,14 +69,10 @@ def harness_camera(n):
     return (n * 1.4, n * 1.15, -0.8 * diag), (n / 2.0, n / 2.0, n / 2.0)
 
 
-def field_terms(n):
-    """Separable smooth field f = 1 + sin(0.4 x s) cos(0.3 y s) + 0.4 sin(0.5 z s), s = 64/n
-    (scaled from test_raycast.py:230-231); range ~[-0.4, 2.4]."""
-    s = 64.0 / n
-    return (lambda x: math.sin(0.4 * x * s)), (lambda y: math.cos(0.3 * y * s)), (lambda z: 0.4 * math.sin(0.5 * z * s))
-
-
-def make_field_torch(n, domain, device, dtype=None):
+def make_field_torch(n, domain, device):
+    """Separable smooth field f = 1 + sin(0.4 x s) cos(0.3 y s) + 0.4 sin(0.5 z s),
+    s = 64/n (scaled from test_raycast.py:230-231); range
+    ~[-0.4, 2.4]; built in 64-slab chunks to bound temporaries."""
     import torch
     g = domain.guard_width
     ox, oy, oz = domain.offset
@@ -475,14 +471,13 @@ def _row_samples(n, image, pos, dirs, step=0.5):
 
 
 def _pick_rows(per_row, budget_samples):
-    import numpy as np
-    order = np.argsort(np.arange(len(per_row)) % 7, kind="stable")   # spread picks over the frame
+    """Every stride-th image row so the sample spans the whole frame and holds
+    about ``budget_samples`` stations."""
     rows, tot = [], 0
     stride = max(1, int(per_row.sum() / max(budget_samples, 1)))
     for r in range(0, len(per_row), stride):
         rows.append(r)
         tot += int(per_row[r])
-    del order
     return rows, tot
 
 

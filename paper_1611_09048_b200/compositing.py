@@ -89,7 +89,7 @@ class DeviceOps:
         return span.contiguous().cpu().numpy().astype("<f4", copy=False).tobytes()
 
     def from_array(self, arr: np.ndarray):
-        return self.torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float32)).to(self.device)
+        return self.torch.from_numpy(np.array(arr, dtype=np.float32)).to(self.device)
 
     def over(self, front, back):
         front, back = front.contiguous(), back.contiguous()

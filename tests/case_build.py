@@ -4,7 +4,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from golden_io import brick_of, cases, gfields
+from golden_io import brick_of, gfields
 from oracle import isaac_oracle as O
 
 

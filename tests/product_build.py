@@ -2,11 +2,9 @@
 
 from __future__ import annotations
 
-import numpy as np
-
 import paper_1611_09048_b200 as P
 from case_build import full_fields
-from golden_io import brick_of, cases, gfields
+from golden_io import gfields
 
 
 def product_scene(c):
