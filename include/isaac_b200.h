@@ -213,8 +213,10 @@ typedef struct {
 ISC_API int isc_binary_swap(const isc_swap_args* args, void* stream);
 /* Number of 8-byte words in a rank's flag block. */
 ISC_API int isc_flag_words(void);
-/* Read-and-clear this rank's transport error word (device -> host, syncs). */
-ISC_API int isc_swap_status(unsigned long long* flags, void* stream, int32_t* out_code);
+/* Read-and-clear this rank's transport error word: stream-ordered copy into
+ * `pinned` (page-locked host memory owned by the caller), then a stream sync. */
+ISC_API int isc_swap_status(unsigned long long* flags, void* stream, unsigned long long* pinned,
+                            int32_t* out_code);
 
 /* Direct-send fallback for non-power-of-two world sizes: rank 0 folds every
  * rank's image (peer loads) in visibility order into root_out; other ranks

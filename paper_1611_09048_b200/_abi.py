@@ -132,7 +132,7 @@ _SIGNATURES = {
     "isc_binary_swap": (C.c_int, [C.POINTER(SwapArgs), C.c_void_p]),
     "isc_direct_send": (C.c_int, [C.POINTER(SwapArgs), C.c_void_p]),
     "isc_flag_words": (C.c_int, []),
-    "isc_swap_status": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int32)]),
+    "isc_swap_status": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int32)]),
     "isc_arena_alloc": (C.c_int, [C.c_size_t, C.POINTER(C.c_void_p)]),
     "isc_arena_free": (C.c_int, [C.c_void_p]),
     "isc_ipc_handle": (C.c_int, [C.c_void_p, C.c_char * IPC_HANDLE_BYTES]),

@@ -261,16 +261,17 @@ extern "C" int isc_direct_send(const isc_swap_args* a, void* stream) {
 
 extern "C" int isc_flag_words(void) { return kFlagWords; }
 
-extern "C" int isc_swap_status(unsigned long long* flags, void* stream, int32_t* out_code) {
-  if (!flags || !out_code) return fail(ISC_E_VALUE, "null argument");
+extern "C" int isc_swap_status(unsigned long long* flags, void* stream, unsigned long long* pinned,
+                               int32_t* out_code) {
+  if (!flags || !out_code || !pinned) return fail(ISC_E_VALUE, "null argument");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  unsigned long long v = 0;
-  ISC_CUDA_CHECK(cudaMemcpyAsync(&v, flags + kErrWord, sizeof(v), cudaMemcpyDeviceToHost, s));
+  // pinned destination: a stream-ordered copy that never waits on other streams
+  ISC_CUDA_CHECK(cudaMemcpyAsync(pinned, flags + kErrWord, sizeof(*pinned), cudaMemcpyDeviceToHost, s));
   ISC_CUDA_CHECK(cudaStreamSynchronize(s));
+  const unsigned long long v = *pinned;
   *out_code = (int32_t)v;
   if (v) {
-    const unsigned long long zero = 0;
-    ISC_CUDA_CHECK(cudaMemcpyAsync(flags + kErrWord, &zero, sizeof(zero), cudaMemcpyHostToDevice, s));
+    ISC_CUDA_CHECK(cudaMemsetAsync(flags + kErrWord, 0, sizeof(unsigned long long), s));
     ISC_CUDA_CHECK(cudaStreamSynchronize(s));
   }
   return ISC_OK;

@@ -305,6 +305,7 @@ class NvlinkTransport(_HostCollectives):
             self.root_out = root_base + self.arena.image_bytes
         self.n_pixels = self.arena.n_pixels
         self.epoch = 0
+        self._status_host = torch.zeros(1, dtype=torch.int64).pin_memory()   # allocated up front
         sms = _abi.lib().isc_device_sm_count(self.arena.device_index)
         self.n_ctas = max(1, sms if sms > 0 else 148)
         self.sent_bytes = 0
@@ -350,7 +351,8 @@ class NvlinkTransport(_HostCollectives):
     def status(self, stream_ptr: int) -> None:
         code = C.c_int32(0)
         self._abi.check(self._abi.lib().isc_swap_status(C.c_void_p(self.flags[self.rank]), C.c_void_p(stream_ptr),
-                                                        C.byref(code)), "swap status")
+                                                        C.c_void_p(self._status_host.data_ptr()), C.byref(code)),
+                        "swap status")
         if code.value:
             raise TransportError(f"rank {self.rank}: peer did not arrive within {self.timeout_s}s "
                                  "(binary swap spin-wait timed out)")
