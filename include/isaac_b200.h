@@ -35,6 +35,7 @@
  *                         and _direct_send           compositing.py:184-194
  *   isc_binary_swap    <- compositing.binary_swap   compositing.py:107-181
  *   isc_to_rgba8       <- runtime.to_rgba8           runtime.py:66-67
+ *   isc_toy_fields     <- harness.ToyState.refresh   harness.py:119-190
  *   isc_arena_* / isc_ipc_* <- transport.Transport  transport.py:20-28
  *                         (the NVLink replacement of LocalFabric queues)
  */
@@ -162,7 +163,7 @@ ISC_API int isc_abi_version(void);
 ISC_API const char* isc_last_error(void);
 /* sizeof of the public structs, so bindings can verify their layouts:
  * which = 0 isc_render_args, 1 isc_source, 2 isc_camera, 3 isc_clip_plane,
- * 4 isc_chain_step, 5 isc_swap_args */
+ * 4 isc_chain_step, 5 isc_swap_args, 6 isc_toy_args */
 ISC_API size_t isc_struct_size(int which);
 ISC_API int isc_device_sm_count(int device);
 
@@ -227,6 +228,24 @@ ISC_API int isc_direct_send(const isc_swap_args* args, void* stream);
 /* out[i] = round_half_even(clip(rgba[i], 0, 1) * 255) per channel, uint8
  * (H, W, 4) -- runtime.to_rgba8 (runtime.py:66-67). */
 ISC_API int isc_to_rgba8(const float* rgba, uint8_t* out, int64_t n_pixels, void* stream);
+
+/* ---- harness field generator ------------------------------------------------ */
+/* Analytic shear-flow fields of the reference harness (harness.ToyState,
+ * harness.py:119-190) for one brick + guard at a given step, float64 math,
+ * float32 output: density (z, y, x) and velocity (z, y, x, 3), either may be
+ * null.  Global coordinates of array index 0 are offset - guard. */
+typedef struct {
+  int32_t global_size[3];
+  int32_t offset[3];
+  int32_t size[3];
+  int32_t guard;
+  int32_t step_index;
+  int32_t seed;
+  double shear_speed, perturbation, dt;
+  float* density;
+  float* velocity;
+} isc_toy_args;
+ISC_API int isc_toy_fields(const isc_toy_args* args, void* stream);
 
 /* ---- device memory shared between processes --------------------------- */
 ISC_API int isc_arena_alloc(size_t bytes, void** out_ptr);     /* cudaMalloc + zero */

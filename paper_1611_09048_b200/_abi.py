@@ -116,6 +116,22 @@ class SwapArgs(C.Structure):
     ]
 
 
+class ToyArgs(C.Structure):
+    _fields_ = [
+        ("global_size", C.c_int32 * 3),
+        ("offset", C.c_int32 * 3),
+        ("size", C.c_int32 * 3),
+        ("guard", C.c_int32),
+        ("step_index", C.c_int32),
+        ("seed", C.c_int32),
+        ("shear_speed", C.c_double),
+        ("perturbation", C.c_double),
+        ("dt", C.c_double),
+        ("density", C.c_void_p),
+        ("velocity", C.c_void_p),
+    ]
+
+
 _lib = None
 _lock = threading.Lock()
 
@@ -140,6 +156,7 @@ _SIGNATURES = {
     "isc_ipc_close": (C.c_int, [C.c_void_p]),
     "isc_enable_peer_access": (C.c_int, [C.c_int]),
     "isc_to_rgba8": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "isc_toy_fields": (C.c_int, [C.POINTER(ToyArgs), C.c_void_p]),
 }
 
 EXPORTED = tuple(_SIGNATURES)
@@ -175,7 +192,7 @@ def lib():
 
 def check_layout(handle=None):
     h = handle or lib()
-    for which, st in enumerate((RenderArgs, Source, Camera, ClipPlane, ChainStep, SwapArgs)):
+    for which, st in enumerate((RenderArgs, Source, Camera, ClipPlane, ChainStep, SwapArgs, ToyArgs)):
         native = h.isc_struct_size(which)
         if native != C.sizeof(st):
             raise NativeLibraryMissing(f"struct {st.__name__}: ctypes {C.sizeof(st)} B != native {native} B")

@@ -35,6 +35,7 @@ extern "C" size_t isc_struct_size(int which) {
     case 3: return sizeof(isc_clip_plane);
     case 4: return sizeof(isc_chain_step);
     case 5: return sizeof(isc_swap_args);
+    case 6: return sizeof(isc_toy_args);
     default: return 0;
   }
 }

@@ -212,6 +212,31 @@ def classify_goldens(seed=99):
     return out, [[list(p) for p in t] for t in tfs]
 
 
+def toy_goldens():
+    """Reference harness fields (ToyState) and whole harness frames (run)."""
+    from insitu import harness as H
+    out = {}
+    cfg = H.HarnessConfig(size=(24, 16, 20), ranks=(2, 1, 1), image_size=(40, 30))
+    vol = cfg.volume()
+    for rank in range(2):
+        dom = vol.local_domain(rank, 1)
+        st = H.ToyState(cfg, dom)
+        for step in (0, 3):
+            st.step_index = step
+            st.refresh()
+            st.fill_scratch()
+            out[f"r{rank}_s{step}_density"] = st.density.copy()
+            out[f"r{rank}_s{step}_velocity"] = st.velocity.copy()
+            out[f"r{rank}_s{step}_scratch"] = st.scratch.copy()
+    frames = {}
+    run_cfg = H.HarnessConfig(size=(32, 32, 32), ranks=(2, 1, 1), steps=3, image_size=(72, 40),
+                              active_sources=(0, 2))
+    H.run(run_cfg, frame_hook=lambda step, img: frames.__setitem__(step, np.array(img)))
+    for step, img in frames.items():
+        out[f"frame_s{step}"] = img
+    return out
+
+
 def main():
     manifest = {"reference": "/root/reference/pkg/src/insitu (insitu 0.1.0)",
                 "numpy": np.__version__, "render": {}, "composite": {}}
@@ -229,6 +254,10 @@ def main():
     arrays, tf_points = classify_goldens()
     np.savez_compressed(os.path.join(HERE, "classify.npz"), **arrays)
     manifest["classify"] = {"file": "classify.npz", "tf_points": tf_points}
+    np.savez_compressed(os.path.join(HERE, "toy.npz"), **toy_goldens())
+    manifest["toy"] = {"file": "toy.npz", "fields_config": {"size": [24, 16, 20], "ranks": [2, 1, 1]},
+                       "run_config": {"size": [32, 32, 32], "ranks": [2, 1, 1], "steps": 3,
+                                      "image_size": [72, 40], "active_sources": [0, 2]}}
     with open(os.path.join(HERE, "manifest.json"), "w") as fh:
         json.dump(manifest, fh, indent=1)
     print("done")

@@ -41,7 +41,7 @@ def test_struct_layouts_and_version():
     assert lib.isc_abi_version() == _abi.ABI_VERSION
     assert lib.isc_flag_words() >= 10
     for which, st in enumerate((_abi.RenderArgs, _abi.Source, _abi.Camera, _abi.ClipPlane, _abi.ChainStep,
-                                _abi.SwapArgs)):
+                                _abi.SwapArgs, _abi.ToyArgs)):
         assert lib.isc_struct_size(which) == C.sizeof(st)
 
 
