@@ -263,7 +263,6 @@ __global__ void __launch_bounds__(kThreads) march_fast_kernel(const __grid_const
   const int th = (PAIRED ? 16 : 32) >> tw_log2;
   const int q = PAIRED ? (lane & 15) : lane;
   const int parity = PAIRED ? (lane >> 4) : 0;
-  const unsigned pair_mask = (1u << lane) | (1u << (lane ^ 16));
 
   for (;;) {
     int t = 0;
@@ -294,11 +293,15 @@ __global__ void __launch_bounds__(kThreads) march_fast_kernel(const __grid_const
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     uint32_t stations = 0;
     if constexpr (PAIRED) {
-      // both lanes of a pair run the same trip count (pair-synchronous shuffles)
+      // Every lane runs the warp's largest trip count so the pair shuffles use
+      // the full mask (a per-lane mask costs a MATCH.ANY convergence check per
+      // shuffle).  Lanes whose ray is finished contribute transparent samples:
+      // over(acc, 0) == acc exactly.
       const long long n = r.hit ? (r.k_hi - r.k_lo) : 0;
-      const long long pairs = (n + 1) >> 1;
-      for (long long j = 0; j < pairs; ++j) {
-        const long long k = r.k_lo + 2 * j + parity;
+      const unsigned pairs = (unsigned)((n + 1) >> 1);
+      const unsigned trips = __reduce_max_sync(0xffffffffu, pairs);
+      for (unsigned j = 0; j < trips; ++j) {
+        const long long k = r.k_lo + 2 * (long long)j + parity;
         float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
         if (k < r.k_hi) {
           double p0[3];
@@ -308,7 +311,7 @@ __global__ void __launch_bounds__(kThreads) march_fast_kernel(const __grid_const
           const float s0 = s.n_steps ? run_chain(s, vv, 1) : v0;
           c = premultiply(classify(lut_s, lo, inv, s0));
         }
-        const float4 other = shfl_pair(c, pair_mask);
+        const float4 other = shfl_pair(c, 0xffffffffu);
         acc = over4(acc, parity ? over4(other, c) : over4(c, other));
       }
       stations = parity ? 0u : (uint32_t)n;
