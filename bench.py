@@ -327,6 +327,8 @@ def run_b200(args):
     e2e = run_e2e(P, torch, dist, ctx, scenes[0], transport, canvas, order, rank, world, red_dev, max(2, k // 2))
 
     norm = time_normalisation(P, torch, reg, domain, peak)
+    host_field = None if args.no_host_field_e2e else run_e2e_host_field(
+        P, torch, dist, ctx, scenes[0], transport, canvas, order, rank, world, red_dev, field)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -350,6 +352,7 @@ def run_b200(args):
                          "kernel": "isc::march_fast_kernel<INTERP=1,GUARDED=1,PAIRED=1>", "kernel_ms": round(kernel_ms_max, 4),
                          "algorithmic_bytes_per_launch": int(br.item() / world)},
             "e2e": e2e,
+            "e2e_host_field": host_field,
             "normalisation": norm,
             "gpu_launches": k * (1 + (1 if world > 1 else 0)),
             "clocks": clk,
@@ -360,6 +363,46 @@ def run_b200(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_e2e_host_field(P, torch, dist, ctx, scene, transport, canvas, order, rank, world, red_dev, field,
+                       steps=3):
+    """Informational: the same public-API frame, but with the brick's field
+    uploaded every step from pinned host memory (a host-resident simulation),
+    plus the frame D2H.  The in-situ contract keeps fields in HBM, so this is
+    not the headline e2e; it shows what PCIe costs when they are not."""
+    host = torch.empty(field.shape, dtype=field.dtype).pin_memory()
+    host.copy_(field)
+    w, h = scene.camera.image_size
+    out = torch.empty((h, w, 4), dtype=torch.float32).pin_memory() if rank == 0 else None
+    stream = torch.cuda.current_stream()
+
+    def one():
+        field.copy_(host, non_blocking=True)
+        img = P.render_local(ctx, scene, out=canvas, check_errors=False)
+        full = P.binary_swap(transport, img.pixels, order)
+        if full is not None:
+            out.copy_(full, non_blocking=True)
+
+    one()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        one()
+    b.record(stream)
+    torch.cuda.synchronize()
+    tt = torch.tensor([a.elapsed_time(b) / steps], dtype=torch.float64, device=red_dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms = float(tt.item())
+    del host
+    return {"value": round(1000.0 / ms, 3), "unit": "frames/s", "ms_per_step": round(ms, 3), "steps": steps,
+            "h2d_bytes_per_step": field.numel() * field.element_size(),
+            "d2h_bytes_per_step": (w * h * 16) if rank == 0 else 0,
+            "note": "field re-uploaded from pinned host memory every frame (not the in-situ case)"}
 
 
 def time_normalisation(P, torch, reg, domain, peak, reps=10):
@@ -595,6 +638,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-step-s", type=float, default=4.0)
     ap.add_argument("--share-gpu", action="store_true", help="test only: all ranks on cuda:0")
+    ap.add_argument("--no-host-field-e2e", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         log("note: warmup < 3 requested; using 3")

@@ -85,8 +85,9 @@ __device__ float3 iso_normal(const isc_source& s, const Brick& b, const double p
   return make_float3(grad[0] / mag, grad[1] / mag, grad[2] / mag);
 }
 
-// FAST: exactly one active float32 scalar source in volume mode.
-template <bool FAST, bool INTERP>
+// Generic fallback: any dtype (f32/f64/f16/bf16), up to ISC_MAX_SOURCES
+// sources, 64-bit element offsets; static 16x16 tiles.
+template <bool INTERP>
 __global__ void __launch_bounds__(kThreads) march_kernel(const __grid_constant__ isc_render_args a) {
   extern __shared__ float4 lut_s[];
   for (int i = threadIdx.x; i < a.n_sources * ISC_LUT_ENTRIES; i += blockDim.x)
@@ -109,21 +110,7 @@ __global__ void __launch_bounds__(kThreads) march_kernel(const __grid_constant__
     const bool gate_alpha = a.alpha_stop < 1.0;
     uint32_t* err = a.error_word;
 
-    if constexpr (FAST) {
-      const isc_source& s = a.src[0];
-      const float lo = s.range_lo, inv = 1.0f / (s.range_hi - s.range_lo);
-      for (long long k = r.k_lo; k < r.k_hi; ++k) {
-        ++stations;
-        double p[3];
-        station_pos(o, r.d, dmul((double)k, a.step), p);
-        const double l[3] = {dsub(p[0], b.offset[0]), dsub(p[1], b.offset[1]), dsub(p[2], b.offset[2])};
-        float v[4];
-        sample_local<true, 1>(s, b, l, INTERP, v, err);
-        const float sc = s.n_steps ? run_chain(s, v, 1) : v[0];
-        acc = over4(acc, premultiply(classify(lut_s, lo, inv, sc)));
-        if (gate_alpha && (double)acc.w >= a.alpha_stop) break;
-      }
-    } else {
+    {
       const int ns = a.n_sources;
       float prev[ISC_MAX_SOURCES];
 #pragma unroll
@@ -492,13 +479,8 @@ extern "C" int isc_render_local(const isc_render_args* a, void* stream) {
   if (!no_multi && launch_multi(a, s, &mstatus)) return mstatus;
   dim3 grid((a->camera.width + kTile - 1) / kTile, (a->camera.height + kTile - 1) / kTile);
   const size_t smem = (size_t)a->n_sources * ISC_LUT_ENTRIES * sizeof(float4);
-  const bool fast = a->n_sources == 1 && a->src[0].feature_dim == 1 && a->src[0].mode == ISC_VOLUME &&
-                    a->src[0].dtype == ISC_F32;
-  const bool interp = a->interpolation != 0;
-  if (fast && interp) march_kernel<true, true><<<grid, kThreads, smem, s>>>(*a);
-  else if (fast) march_kernel<true, false><<<grid, kThreads, smem, s>>>(*a);
-  else if (interp) march_kernel<false, true><<<grid, kThreads, smem, s>>>(*a);
-  else march_kernel<false, false><<<grid, kThreads, smem, s>>>(*a);
+  if (a->interpolation) march_kernel<true><<<grid, kThreads, smem, s>>>(*a);
+  else march_kernel<false><<<grid, kThreads, smem, s>>>(*a);
   ISC_CUDA_CHECK(cudaGetLastError());
   return ISC_OK;
 }
