@@ -94,6 +94,41 @@ __global__ void fold_kernel(float4* out, const __grid_constant__ FoldArgs f, lon
   }
 }
 
+// out[i] = front/back over of mine[i] and theirs[i] for i in [c0, c1): 4
+// pixels (8 independent 16-byte loads) per thread in flight.
+__device__ __forceinline__ void over_span(float4* mine, const float4* theirs, long long c0, long long c1,
+                                          bool partner_front) {
+  const long long stride = blockDim.x;
+  long long i = c0 + threadIdx.x;
+  for (; i + 3 * stride < c1; i += 4 * stride) {
+    float4 m[4], t[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      m[u] = __ldcg(mine + i + u * stride);
+      t[u] = __ldcg(theirs + i + u * stride);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) mine[i + u * stride] = partner_front ? over4(t[u], m[u]) : over4(m[u], t[u]);
+  }
+  for (; i < c1; i += stride) {
+    const float4 m = __ldcg(mine + i), t = __ldcg(theirs + i);
+    mine[i] = partner_front ? over4(t, m) : over4(m, t);
+  }
+}
+
+__device__ __forceinline__ void copy_span(float4* out, const float4* in, long long c0, long long c1) {
+  const long long stride = blockDim.x;
+  long long i = c0 + threadIdx.x;
+  for (; i + 3 * stride < c1; i += 4 * stride) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldcg(in + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) out[i + u * stride] = v[u];
+  }
+  for (; i < c1; i += stride) out[i] = __ldcg(in + i);
+}
+
 __device__ __forceinline__ void cta_chunk(long long lo, long long hi, long long& a, long long& b) {
   const long long n = hi - lo;
   const long long per = (n + gridDim.x - 1) / gridDim.x;
@@ -129,11 +164,7 @@ __global__ void __launch_bounds__(512) swap_kernel(const __grid_constant__ isc_s
       const float4* theirs = reinterpret_cast<const float4*>(a.image[partner]);
       long long c0, c1;
       cta_chunk(klo, khi, c0, c1);
-      const bool partner_front = pv < v;
-      for (long long i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
-        const float4 m = __ldcg(mine + i), t = __ldcg(theirs + i);
-        mine[i] = partner_front ? over4(t, m) : over4(m, t);
-      }
+      over_span(mine, theirs, c0, c1, pv < v);
       publish(me, r + 1);
     }
     lo = klo;
@@ -145,7 +176,7 @@ __global__ void __launch_bounds__(512) swap_kernel(const __grid_constant__ isc_s
     float4* out = reinterpret_cast<float4*>(a.root_out);
     long long c0, c1;
     cta_chunk(lo, hi, c0, c1);
-    for (long long i = c0 + threadIdx.x; i < c1; i += blockDim.x) out[i] = __ldcg(mine + i);
+    copy_span(out, mine, c0, c1);
     publish(me, rounds + 1);
   }
 
