@@ -449,7 +449,7 @@ def run_e2e(P, torch, dist, ctx, scene, transport, canvas, order, rank, world, r
         i = counter[0] % 2
         counter[0] += 1
         sc = P.SceneState.from_bytes(payload)          # scene as received from the root
-        LUTS._cache.clear()                             # force this step's LUT upload
+        LUTS.clear()                                    # force this step's LUT upload
         img = P.render_local(ctx, sc, out=canvas, check_errors=False)
         full = P.binary_swap(transport, img.pixels, order)
         if full is not None:

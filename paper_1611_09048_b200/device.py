@@ -4,6 +4,7 @@ for device memory and streams only; every computation goes through the C-ABI."""
 from __future__ import annotations
 
 import ctypes as C
+import threading
 from collections import OrderedDict
 
 import numpy as np
@@ -54,22 +55,29 @@ class LutCache:
 
     def __init__(self, capacity: int = 64):
         self._cache: "OrderedDict[tuple, torch.Tensor]" = OrderedDict()
+        self._lock = threading.Lock()       # rank threads share one cache
         self.capacity = capacity
         self.uploads = 0
 
     def get(self, lut: np.ndarray, device: torch.device) -> torch.Tensor:
         host = np.ascontiguousarray(lut, dtype=np.float32)
         key = (device.index, host.tobytes())
-        t = self._cache.get(key)
-        if t is not None:
-            self._cache.move_to_end(key)
-            return t
+        with self._lock:
+            t = self._cache.get(key)
+            if t is not None:
+                self._cache.move_to_end(key)
+                return t
         t = torch.from_numpy(host).to(device)
-        self.uploads += 1
-        self._cache[key] = t
-        if len(self._cache) > self.capacity:
-            self._cache.popitem(last=False)
+        with self._lock:
+            self.uploads += 1
+            self._cache[key] = t
+            if len(self._cache) > self.capacity:
+                self._cache.popitem(last=False)
         return t
+
+    def clear(self) -> None:
+        with self._lock:
+            self._cache.clear()
 
 
 LUTS = LutCache()
