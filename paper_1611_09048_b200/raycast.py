@@ -250,6 +250,11 @@ def render_local(rank_ctx, scene: SceneState, plans: Optional[Sequence[SourcePla
         img.check()
     if station_recorder is not None:
         _replay_stations(station_recorder, counts, kr)
+    # tensors the launch reads (staged fields, LUTs) stay alive for the
+    # allocator until this stream has passed the kernel
+    run_stream = stream if stream is not None else torch.cuda.current_stream()
+    for t in keep:
+        t.record_stream(run_stream)
     keep.clear()
     return img
 
