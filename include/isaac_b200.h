@@ -109,6 +109,13 @@ typedef struct {
   int32_t n_steps;           /* chain length (0 = identity)               */
   const float* lut;          /* device, 256 x 4 straight RGBA (float32)  */
   isc_chain_step steps[ISC_MAX_CHAIN];
+  /* Optional analytic form of the LUT: when the 256 entries lie on one
+   * straight run (e.g. a two-point ramp), lut_linear = 1 and
+   * lut(x) = lut_base + lut_slope * x for x = 255 t exactly as the LUT lerp
+   * would give it; the kernel then skips the shared-memory lookup. */
+  int32_t lut_linear;
+  float lut_base[4];
+  float lut_slope[4];
 } isc_source;
 
 /* Camera in global cell coordinates; basis/tan/aspect precomputed on the

@@ -50,6 +50,9 @@ class Source(C.Structure):
         ("n_steps", C.c_int32),
         ("lut", C.c_void_p),
         ("steps", ChainStep * MAX_CHAIN),
+        ("lut_linear", C.c_int32),
+        ("lut_base", C.c_float * 4),
+        ("lut_slope", C.c_float * 4),
     ]
 
 

@@ -228,7 +228,16 @@ __global__ void __launch_bounds__(kThreads) march_kernel(const __grid_constant__
 // order with one shuffle exchange: pair = s_even over s_odd, acc = acc over
 // pair -- the same over-sequence as the reference's per-station loop.
 // Used when early termination is off (alpha_stop >= 1).
-template <bool INTERP, bool GUARDED, bool PAIRED>
+// Straight RGBA of a transfer function whose LUT is one straight run
+// (isc_source.lut_linear): identical to the LUT lerp, no shared-memory lookup.
+__device__ __forceinline__ float4 classify_line(const isc_source& s, float lo, float inv_span, float v) {
+  if (!isfinite(v)) return make_float4(0.f, 0.f, 0.f, 0.f);
+  const float x = fminf(fmaxf((v - lo) * inv_span, 0.0f), 1.0f) * (float)(ISC_LUT_ENTRIES - 1);
+  return make_float4(fmaf(s.lut_slope[0], x, s.lut_base[0]), fmaf(s.lut_slope[1], x, s.lut_base[1]),
+                     fmaf(s.lut_slope[2], x, s.lut_base[2]), fmaf(s.lut_slope[3], x, s.lut_base[3]));
+}
+
+template <bool INTERP, bool GUARDED, bool PAIRED, bool LINE = false>
 __global__ void __launch_bounds__(kThreads) march_fast_kernel(const __grid_constant__ isc_render_args a,
                                                               const FastField F, int tiles_x, int tiles_y,
                                                               int super_x, int n_codes, int row_order,
@@ -296,7 +305,7 @@ __global__ void __launch_bounds__(kThreads) march_fast_kernel(const __grid_const
           const float v0 = fast_sample<INTERP, GUARDED>(F, p0, err);
           float vv[4] = {v0, 0.f, 0.f, 0.f};
           const float s0 = s.n_steps ? run_chain(s, vv, 1) : v0;
-          c = premultiply(classify(lut_s, lo, inv, s0));
+          c = premultiply(LINE ? classify_line(s, lo, inv, s0) : classify(lut_s, lo, inv, s0));
         }
         const float4 other = shfl_pair(c, 0xffffffffu);
         acc = over4(acc, parity ? over4(other, c) : over4(c, other));
@@ -434,7 +443,7 @@ static bool fast_eligible(const isc_render_args* a, FastField& F) {
   return true;
 }
 
-template <bool INTERP, bool GUARDED, bool PAIRED>
+template <bool INTERP, bool GUARDED, bool PAIRED, bool LINE = false>
 static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_t st) {
   static const int tw_log2 = getenv("ISC_TILE_W") ? __builtin_ctz(atoi(getenv("ISC_TILE_W"))) : 3;
   const int tw = 1 << tw_log2, th = (PAIRED ? 16 : 32) >> tw_log2;
@@ -445,12 +454,12 @@ static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_
   int dev = 0, sms = 148, per_sm = 1;
   ISC_CUDA_CHECK(cudaGetDevice(&dev));
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_fast_kernel<INTERP, GUARDED, PAIRED>, kThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_fast_kernel<INTERP, GUARDED, PAIRED, LINE>, kThreads, 0);
   const int total_warps = (n_codes + 0);
   int grid = sms * (per_sm > 0 ? per_sm : 1);
   const int need = (total_warps + (kThreads / 32) - 1) / (kThreads / 32);
   if (grid > need) grid = need > 0 ? need : 1;
-  march_fast_kernel<INTERP, GUARDED, PAIRED><<<grid, kThreads, 0, st>>>(*a, F, tiles_x, tiles_y, super_x, n_codes, row_order ? 1 : 0,
+  march_fast_kernel<INTERP, GUARDED, PAIRED, LINE><<<grid, kThreads, 0, st>>>(*a, F, tiles_x, tiles_y, super_x, n_codes, row_order ? 1 : 0,
                                                                  tw_log2);
   ISC_CUDA_CHECK(cudaGetLastError());
   return ISC_OK;
@@ -470,6 +479,7 @@ extern "C" int isc_render_local(const isc_render_args* a, void* stream) {
     const bool guarded = interp && a->src[0].has_guard;
     static const bool no_pair = getenv("ISC_DISABLE_PAIRED") != nullptr;
     const bool paired = !no_pair && a->alpha_stop >= 1.0;
+    if (interp && guarded && paired && a->src[0].lut_linear) return launch_fast<true, true, true, true>(a, F, s);
     if (interp && guarded) return paired ? launch_fast<true, true, true>(a, F, s) : launch_fast<true, true, false>(a, F, s);
     if (interp) return paired ? launch_fast<true, false, true>(a, F, s) : launch_fast<true, false, false>(a, F, s);
     return paired ? launch_fast<false, false, true>(a, F, s) : launch_fast<false, false, false>(a, F, s);

@@ -126,7 +126,7 @@ def _strides(t: torch.Tensor):
 
 
 def pack_render_args(domain, volume, scene: SceneState, plans: Sequence[SourcePlan], device,
-                     keep: list) -> _abi.RenderArgs:
+                     keep: list, analytic_lut: bool = True) -> _abi.RenderArgs:
     """Fill an ``isc_render_args`` block.  ``keep`` collects the tensors whose
     device pointers the block references (they must outlive the launch)."""
     a = _abi.RenderArgs()
@@ -190,6 +190,11 @@ def pack_render_args(domain, volume, scene: SceneState, plans: Sequence[SourcePl
         lut = LUTS.get(plan.tf.lut, device)
         keep.append(lut)
         s.lut = ptr(lut)
+        line = lut_line(plan.tf.lut) if analytic_lut else None
+        if line is not None:
+            s.lut_linear = 1
+            s.lut_base[:] = [float(v) for v in line[0]]
+            s.lut_slope[:] = [float(v) for v in line[1]]
         prog = device_program(plan.chain)
         s.n_steps = len(prog)
         for j, (op, in_dim, arg) in enumerate(prog):
@@ -199,10 +204,25 @@ def pack_render_args(domain, volume, scene: SceneState, plans: Sequence[SourcePl
     return a
 
 
+def lut_line(lut: np.ndarray, tol: float = 1e-12):
+    """(base, slope) if all 256 LUT entries lie on one line in x = 0..255
+    (so the LUT lerp equals base + slope * x), else None."""
+    lut = np.asarray(lut, dtype=np.float64)
+    second = lut[2:] - 2.0 * lut[1:-1] + lut[:-2]
+    if np.abs(second).max() > tol:
+        return None
+    slope = (lut[-1] - lut[0]) / (lut.shape[0] - 1)
+    base = lut[0]
+    fit = base[None, :] + slope[None, :] * np.arange(lut.shape[0])[:, None]
+    if np.abs(fit - lut).max() > 1e-9:
+        return None
+    return base, slope
+
+
 def render_local(rank_ctx, scene: SceneState, plans: Optional[Sequence[SourcePlan]] = None,
                  station_recorder: Optional[StationRecorder] = None, *, out: Optional[torch.Tensor] = None,
                  stream=None, check_errors: bool = True, keep_station_counts: bool = False,
-                 keep_krange: bool = False, events=None) -> LocalImage:
+                 keep_krange: bool = False, events=None, analytic_lut: bool = True) -> LocalImage:
     """Render the rank's brick into a partial image (raycast.py:492-541).
 
     ``out`` (optional) is a caller-owned CUDA float32 (H, W, 4) tensor to
@@ -210,6 +230,8 @@ def render_local(rank_ctx, scene: SceneState, plans: Optional[Sequence[SourcePla
     ``binary_swap``).  ``check_errors=False`` skips the synchronising guard
     check; call ``LocalImage.check()`` later instead.  ``events`` = (start,
     end) CUDA events recorded around the kernel launch (bench timing).
+    ``analytic_lut=False`` forces the shared-memory LUT lookup even for
+    single-ramp transfer functions (see ``lut_line``).
     """
     device = require_cuda()
     domain, volume = rank_ctx.domain, rank_ctx.global_volume
@@ -217,7 +239,7 @@ def render_local(rank_ctx, scene: SceneState, plans: Optional[Sequence[SourcePla
         plans = build_plans(rank_ctx.registry, rank_ctx.functor_registry, rank_ctx.limits, scene)
     w, h = scene.camera.image_size
     keep: list = []
-    args = pack_render_args(domain, volume, scene, plans, device, keep)
+    args = pack_render_args(domain, volume, scene, plans, device, keep, analytic_lut)
     if out is None:
         out = torch.empty((h, w, 4), dtype=torch.float32, device=device)
     elif out.shape != (h, w, 4) or out.dtype != torch.float32 or not out.is_contiguous() or out.device != device:

@@ -332,3 +332,23 @@ def test_numpy_and_sampler_sources_are_staged():
         fr = P.default_registry()
         out.append(P.render_local(P.RankContext(vol, dom, reg, fr, fr.limits), scene).pixels.cpu().numpy())
     assert np.array_equal(out[0], out[1]) and np.array_equal(out[0], out[2])
+
+
+def test_analytic_single_ramp_classification_equals_lut_path():
+    """A transfer function whose LUT is one straight run is classified as
+    base + slope * x; the result matches the shared-memory LUT path and the
+    oracle, and non-ramp TFs never take the shortcut."""
+    import paper_1611_09048_b200 as P
+    from paper_1611_09048_b200.raycast import lut_line
+    from product_build import product_ctx, product_scene
+    c = cases.case("c1")
+    gold = load("render_c1.npz")
+    ctx = product_ctx(c, (1, 1, 1), 0)
+    scene = product_scene(c)
+    assert lut_line(scene.transfer_function(0).lut) is not None
+    fast = P.render_local(ctx, scene).pixels.cpu().numpy()
+    lut = P.render_local(ctx, scene, analytic_lut=False).pixels.cpu().numpy()
+    assert np.abs(fast - lut).max() <= 2e-6
+    assert np.abs(fast - gold["d111_r0_rgba"]).max() <= RGBA_TOL
+    warm = P.tf_from_points(cases.WARM_TF, (0.0, 1.0))
+    assert lut_line(warm.lut) is None
