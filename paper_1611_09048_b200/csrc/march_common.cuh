@@ -19,9 +19,20 @@ struct FastField {
   int g;
 };
 
+// floor(p) as an exact double and as an int without conversion instructions:
+// rounding p + 1.5*2^52 toward -inf leaves floor(p) in the low mantissa bits
+// (exact for |p| < 2^51), so the XU pipe only sees the final float conversion.
+__device__ __forceinline__ double floor_split(double p, int& i) {
+  constexpr double kMagic = 6755399441055744.0;  // 2^52 + 2^51
+  const double t = __dadd_rd(p, kMagic);
+  i = __double2loint(t);
+  return __dsub_rn(t, kMagic);
+}
+
 template <bool INTERP, bool GUARDED>
 __device__ __forceinline__ float fast_sample(const FastField& F, const double p[3], uint32_t* err) {
-  int ix = __double2int_rd(p[0]), iy = __double2int_rd(p[1]), iz = __double2int_rd(p[2]);
+  int ix, iy, iz;
+  const double flx = floor_split(p[0], ix), fly = floor_split(p[1], iy), flz = floor_split(p[2], iz);
   if constexpr (!INTERP) {
     // nearest: clamp the local cell into the brick (fields.py:240-242)
     const int x = min(max(ix - F.lo[0] - F.g, 0), F.hi[0]) + F.g;
@@ -29,8 +40,7 @@ __device__ __forceinline__ float fast_sample(const FastField& F, const double p[
     const int z = min(max(iz - F.lo[2] - F.g, 0), F.hi[2]) + F.g;
     return __ldg(F.f + (z * F.sz + y * F.sy + x * F.sx));
   } else {
-    const float fx = (float)dsub(p[0], (double)ix), fy = (float)dsub(p[1], (double)iy),
-                fz = (float)dsub(p[2], (double)iz);
+    const float fx = (float)dsub(p[0], flx), fy = (float)dsub(p[1], fly), fz = (float)dsub(p[2], flz);
     int x0, y0, z0, dx, dy, dz;
     if constexpr (GUARDED) {
       x0 = ix - F.lo[0];

@@ -89,12 +89,10 @@ __device__ __forceinline__ void multi_sample(const MultiSrc& S, const MultiField
 
 __device__ __forceinline__ void cell_of(const double p[3], int& ix, int& iy, int& iz, float& fx, float& fy,
                                         float& fz) {
-  ix = __double2int_rd(p[0]);
-  iy = __double2int_rd(p[1]);
-  iz = __double2int_rd(p[2]);
-  fx = (float)dsub(p[0], (double)ix);
-  fy = (float)dsub(p[1], (double)iy);
-  fz = (float)dsub(p[2], (double)iz);
+  const double flx = floor_split(p[0], ix), fly = floor_split(p[1], iy), flz = floor_split(p[2], iz);
+  fx = (float)dsub(p[0], flx);
+  fy = (float)dsub(p[1], fly);
+  fz = (float)dsub(p[2], flz);
 }
 
 // Chained scalar of one source at an arbitrary global position (iso extras).
