@@ -14,7 +14,7 @@ import threading
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libisaac_b200.so")
+LIB_PATH = os.environ.get("ISC_LIB_PATH") or os.path.join(_HERE, "lib", "libisaac_b200.so")
 
 ABI_VERSION = 1
 MAX_SOURCES = 8

@@ -230,15 +230,20 @@ __global__ void __launch_bounds__(kThreads) march_kernel(const __grid_constant__
 // Used when early termination is off (alpha_stop >= 1).
 // Straight RGBA of a transfer function whose LUT is one straight run
 // (isc_source.lut_linear): identical to the LUT lerp, no shared-memory lookup.
-__device__ __forceinline__ float4 classify_line(const isc_source& s, float lo, float inv_span, float v) {
-  if (!isfinite(v)) return make_float4(0.f, 0.f, 0.f, 0.f);
+// Returns the PREMULTIPLIED colour; a non-finite value gets alpha 0 (and so
+// rgb 0) through a select instead of a branch.
+__device__ __forceinline__ float4 classify_line_premul(const isc_source& s, float lo, float inv_span, float v) {
   const float x = fminf(fmaxf((v - lo) * inv_span, 0.0f), 1.0f) * (float)(ISC_LUT_ENTRIES - 1);
-  return make_float4(fmaf(s.lut_slope[0], x, s.lut_base[0]), fmaf(s.lut_slope[1], x, s.lut_base[1]),
-                     fmaf(s.lut_slope[2], x, s.lut_base[2]), fmaf(s.lut_slope[3], x, s.lut_base[3]));
+  const float a = isfinite(v) ? fmaf(s.lut_slope[3], x, s.lut_base[3]) : 0.0f;
+  return make_float4(fmaf(s.lut_slope[0], x, s.lut_base[0]) * a, fmaf(s.lut_slope[1], x, s.lut_base[1]) * a,
+                     fmaf(s.lut_slope[2], x, s.lut_base[2]) * a, a);
 }
 
+#ifndef ISC_FAST_MINB
+#define ISC_FAST_MINB 4  // <= 64 registers: 4 CTAs (32 warps) per SM
+#endif
 template <bool INTERP, bool GUARDED, bool PAIRED, bool LINE = false>
-__global__ void __launch_bounds__(kThreads) march_fast_kernel(const __grid_constant__ isc_render_args a,
+__global__ void __launch_bounds__(kThreads, ISC_FAST_MINB) march_fast_kernel(const __grid_constant__ isc_render_args a,
                                                               const FastField F, int tiles_x, int tiles_y,
                                                               int super_x, int n_codes, int row_order,
                                                               int tw_log2) {
@@ -294,21 +299,49 @@ __global__ void __launch_bounds__(kThreads) march_fast_kernel(const __grid_const
       // shuffle).  Lanes whose ray is finished contribute transparent samples:
       // over(acc, 0) == acc exactly.
       const long long n = r.hit ? (r.k_hi - r.k_lo) : 0;
-      const unsigned pairs = (unsigned)((n + 1) >> 1);
+      long long nm = n;  // stations this lane pair marches
+#ifndef ISC_EXP_SAMPLE_GUARD
+      // Guard contract checked once per ray: every axis of the station
+      // position o + (k*step)*d is a composition of monotone roundings, so
+      // each cell index is monotone in k and the base cells of the first and
+      // last station bound those of every station between them.  A violating
+      // ray is not marched (the call reports GuardContractError, as the
+      // reference raises on the first bad gather, fields.py:230-238).
+      if (GUARDED && n > 0) {
+        double pa[3], pb[3];
+        station_pos(o, r.d, dmul((double)r.k_lo, step), pa);
+        station_pos(o, r.d, dmul((double)(r.k_hi - 1), step), pb);
+        if (!guard_ok(F, pa) || !guard_ok(F, pb)) {
+          if (err && !parity) atomicAdd(err, 1u);
+          nm = 0;
+        }
+      }
+      constexpr bool kCheck = false;
+#else
+      constexpr bool kCheck = true;
+#endif
+      const unsigned pairs = (unsigned)((nm + 1) >> 1);
       const unsigned trips = __reduce_max_sync(0xffffffffu, pairs);
-      for (unsigned j = 0; j < trips; ++j) {
-        const long long k = r.k_lo + 2 * (long long)j + parity;
+      // station index as an exact float64 integer (k < 2^53) stepped by 2.0:
+      // no int64 -> float64 conversion per sample; `left` counts this lane's
+      // remaining stations.
+      double kd = (double)(r.k_lo + parity);
+      int left = (int)nm - parity;
+      for (unsigned j = 0; j < trips; ++j, left -= 2, kd = dadd(kd, 2.0)) {
         float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (k < r.k_hi) {
+        if (left > 0) {
           double p0[3];
-          station_pos(o, r.d, dmul((double)k, step), p0);
-          const float v0 = fast_sample<INTERP, GUARDED>(F, p0, err);
+          station_pos(o, r.d, dmul(kd, step), p0);
+          const float v0 = fast_sample<INTERP, GUARDED, kCheck>(F, p0, err);
           float vv[4] = {v0, 0.f, 0.f, 0.f};
           const float s0 = s.n_steps ? run_chain(s, vv, 1) : v0;
-          c = premultiply(LINE ? classify_line(s, lo, inv, s0) : classify(lut_s, lo, inv, s0));
+          c = LINE ? classify_line_premul(s, lo, inv, s0) : premultiply(classify(lut_s, lo, inv, s0));
         }
-        const float4 other = shfl_pair(c, 0xffffffffu);
-        acc = over4(acc, parity ? over4(other, c) : over4(c, other));
+        // Only the even lane's accumulator is used (it writes the pixel), so
+        // it takes the odd lane's sample with a shuffle-down and composites
+        // even-over-odd; the odd lane's accumulator is dead.
+        const float4 odd = shfl_down16(c);
+        acc = over4(acc, over4(c, odd));
       }
       stations = parity ? 0u : (uint32_t)n;
       if (parity || !in_img) {

@@ -29,7 +29,20 @@ __device__ __forceinline__ double floor_split(double p, int& i) {
   return __dsub_rn(t, kMagic);
 }
 
-template <bool INTERP, bool GUARDED>
+// Guard contract of a trilinear gather at p (fields.py:218-238): the base
+// cell must lie in [0, hi] of the guarded array on every axis.
+__device__ __forceinline__ bool guard_ok(const FastField& F, const double p[3]) {
+  int ix, iy, iz;
+  floor_split(p[0], ix);
+  floor_split(p[1], iy);
+  floor_split(p[2], iz);
+  return (unsigned)(ix - F.lo[0]) <= (unsigned)F.hi[0] && (unsigned)(iy - F.lo[1]) <= (unsigned)F.hi[1] &&
+         (unsigned)(iz - F.lo[2]) <= (unsigned)F.hi[2];
+}
+
+// CHECK = false: the caller has proven the guard contract for this sample
+// (see march_fast_kernel: endpoint check per ray).
+template <bool INTERP, bool GUARDED, bool CHECK = true>
 __device__ __forceinline__ float fast_sample(const FastField& F, const double p[3], uint32_t* err) {
   int ix, iy, iz;
   const double flx = floor_split(p[0], ix), fly = floor_split(p[1], iy), flz = floor_split(p[2], iz);
@@ -46,7 +59,8 @@ __device__ __forceinline__ float fast_sample(const FastField& F, const double p[
       x0 = ix - F.lo[0];
       y0 = iy - F.lo[1];
       z0 = iz - F.lo[2];
-      if ((unsigned)x0 > (unsigned)F.hi[0] || (unsigned)y0 > (unsigned)F.hi[1] || (unsigned)z0 > (unsigned)F.hi[2]) {
+      if (CHECK &&
+          ((unsigned)x0 > (unsigned)F.hi[0] || (unsigned)y0 > (unsigned)F.hi[1] || (unsigned)z0 > (unsigned)F.hi[2])) {
         if (err) atomicAdd(err, 1u);
         x0 = min(max(x0, 0), F.hi[0]);
         y0 = min(max(y0, 0), F.hi[1]);
@@ -83,12 +97,10 @@ __device__ __forceinline__ int morton3(int w, int shift) {
   return ((w >> shift) & 1) | (((w >> (shift + 2)) & 1) << 1) | (((w >> (shift + 4)) & 1) << 2);
 }
 
-// Exchange with lane ^ 16 only: the two lanes of a pair run identical trip
-// counts, other pairs of the warp may already have left the loop.
-__device__ __forceinline__ float4 shfl_pair(float4 v, unsigned mask) {
-  return make_float4(__shfl_xor_sync(mask, v.x, 16), __shfl_xor_sync(mask, v.y, 16),
-                     __shfl_xor_sync(mask, v.z, 16), __shfl_xor_sync(mask, v.w, 16));
+// Lanes 0-15 receive lane + 16's value (full mask; lanes 16-31 get their own).
+__device__ __forceinline__ float4 shfl_down16(float4 v) {
+  return make_float4(__shfl_down_sync(0xffffffffu, v.x, 16), __shfl_down_sync(0xffffffffu, v.y, 16),
+                     __shfl_down_sync(0xffffffffu, v.z, 16), __shfl_down_sync(0xffffffffu, v.w, 16));
 }
-
 
 }  // namespace isc

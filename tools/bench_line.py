@@ -1,9 +1,9 @@
-"""Print the key fields of the bench JSON line(s) in a file: tools/bench_line.py FILE [label]."""
+"""Print the key fields of the bench JSON line(s) in a file: tools/bench_line.py [FILE|-] [label]."""
 import json
 import sys
 
 label = sys.argv[2] if len(sys.argv) > 2 else ""
-for line in open(sys.argv[1]):
+for line in (open(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1] != "-" else sys.stdin):
     line = line.strip()
     if not line.startswith("{"):
         continue

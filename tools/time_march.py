@@ -1,0 +1,62 @@
+"""Time the march kernel alone (CUDA events, field resident) for one BASELINE
+config: python tools/time_march.py [--config c4] [--reps 20].  With
+ISC_LIB_PATH set it times that library build (A/B experiments)."""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_1611_09048_b200 as P  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--lut", action="store_true", help="force the shared-memory LUT path")
+    args = ap.parse_args()
+    cfg = bench.CONFIGS[args.config]
+    n = cfg["n"]
+    vol = P.GlobalVolume((n,) * 3, (1, 1, 1))
+    dom = vol.local_domain(0, 1)
+    field = bench.make_field_torch(n, dom, "cuda")
+    reg = P.SourceRegistry(dom)
+    reg.register_handle(P.array_backed_handle(P.SourceDescriptor("density", 1, has_guard=True), field, 1))
+    active = {0}
+    if cfg.get("multi"):
+        reg.register_handle(P.array_backed_handle(P.SourceDescriptor("velocity", 3, has_guard=True),
+                                                  bench.make_vector_field_torch(n, dom, "cuda"), 1))
+        active = {0, 1}
+    P.update_sources(reg, active, {})
+    fr = P.default_registry()
+    ctx = P.RankContext(vol, dom, reg, fr, fr.limits)
+    scene = bench.build_scene(P, cfg)
+    w, h = cfg["image"]
+    out = torch.empty((h, w, 4), dtype=torch.float32, device="cuda")
+    plans = P.build_plans(reg, fr, fr.limits, scene)
+    kw = dict(plans=plans, out=out, check_errors=False)
+    if args.lut:
+        kw["analytic_lut"] = False
+    for _ in range(3):
+        img = P.render_local(ctx, scene, **kw)
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.reps)]
+    for e in evs:
+        P.render_local(ctx, scene, events=e, **kw)
+    torch.cuda.synchronize()
+    ms = sorted(a.elapsed_time(b) for a, b in evs)
+    res = {"lib": os.environ.get("ISC_LIB_PATH", "default"), "config": args.config, "median_ms": round(ms[len(ms) // 2], 4),
+           "min_ms": round(ms[0], 4), "stations": int(img.stations)}
+    chk = out.double().sum().item()
+    res["checksum"] = round(chk, 3)
+    print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()
