@@ -11,6 +11,8 @@
 // unrolled at compile time (NS = 1..4) so per-source iso state lives in
 // registers.  Iso side-samples (entry pair, exit pair, 6 gradient taps) are
 // rare and go through one out-of-line point sampler.
+#include <cstdlib>
+
 #include "march_common.cuh"
 #include "sample.cuh"
 
@@ -286,6 +288,272 @@ __global__ void __launch_bounds__(kThreads, MINB) march_multi_kernel(const __gri
   }
 }
 
+// ---------------------------------------------------------------------------
+// Specialised multi-source march: trilinear, every source guarded
+// (has_guard), component counts known at compile time (DIMS packs one base-5
+// digit per source).  Versus march_multi_kernel: the guard contract is proven
+// once per ray from its end stations (cell indices are monotone in k, see
+// march_fast_kernel), so the per-station gathers of all sources carry no
+// checks or clamps and are issued back to back; component loops are fully
+// unrolled.  A ray whose end station fails the check is marched with the
+// per-station check instead: an iso hit or early termination may stop it
+// before the bad station, and the reference only raises on a gather it
+// performs.  Iso side samples reuse the generic out-of-line point sampler.
+template <int DIMS, int SI>
+__host__ __device__ constexpr int dim_at() {
+  return SI == 0 ? DIMS % 5 : SI == 1 ? (DIMS / 5) % 5 : SI == 2 ? (DIMS / 25) % 5 : (DIMS / 125) % 5;
+}
+
+template <int D>
+__device__ __forceinline__ void gather_guarded(const MultiSrc& S, int x0, int y0, int z0, float fx, float fy,
+                                               float fz, float v[4]) {
+  const float* b = S.f + (z0 * S.sz + y0 * S.sy + x0 * S.sx);
+  const int dx = S.sx, dy = S.sy, dz = S.sz;
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    const float* p = b + c * S.sc;
+    const float v000 = __ldg(p), v100 = __ldg(p + dx), v010 = __ldg(p + dy), v110 = __ldg(p + dy + dx);
+    const float* q = p + dz;
+    const float v001 = __ldg(q), v101 = __ldg(q + dx), v011 = __ldg(q + dy), v111 = __ldg(q + dy + dx);
+    const float a0 = fmaf(fx, v100 - v000, v000), a1 = fmaf(fx, v110 - v010, v010);
+    const float a2 = fmaf(fx, v101 - v001, v001), a3 = fmaf(fx, v111 - v011, v011);
+    const float b0 = fmaf(fy, a1 - a0, a0), b1 = fmaf(fy, a3 - a2, a2);
+    v[c] = fmaf(fz, b1 - b0, b0);
+  }
+}
+
+__device__ __forceinline__ bool cell_guard_ok(const MultiField& M, const double p[3]) {
+  int ix, iy, iz;
+  floor_split(p[0], ix);
+  floor_split(p[1], iy);
+  floor_split(p[2], iz);
+  const MultiSrc& S = M.s[0];  // every source of this kernel is guarded: same halo bounds
+  return (unsigned)(ix - M.lo[0]) <= (unsigned)S.hi[0] && (unsigned)(iy - M.lo[1]) <= (unsigned)S.hi[1] &&
+         (unsigned)(iz - M.lo[2]) <= (unsigned)S.hi[2];
+}
+
+#ifndef ISC_MULTI_FAST_MINB
+#define ISC_MULTI_FAST_MINB 2
+#endif
+
+template <int NS, int DIMS>
+__global__ void __launch_bounds__(kThreads, ISC_MULTI_FAST_MINB)
+    march_multi_fast_kernel(const __grid_constant__ isc_render_args a, const __grid_constant__ MultiField M,
+                            int tiles_x, int tiles_y, int super_x, int n_codes) {
+  __shared__ float4 lut_s[NS * ISC_LUT_ENTRIES];
+  for (int i = threadIdx.x; i < NS * ISC_LUT_ENTRIES; i += blockDim.x)
+    lut_s[i] = reinterpret_cast<const float4*>(a.src[i >> 8].lut)[i & (ISC_LUT_ENTRIES - 1)];
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31;
+  const bool gate_alpha = a.alpha_stop < 1.0;
+  const double* o = a.camera.origin;
+  const double step = a.step;
+  uint32_t* err = a.error_word;
+  unsigned long long warp_stations = 0;
+
+  for (;;) {
+    int t = 0;
+    if (lane == 0) t = (int)atomicAdd(a.work_counter, 1u);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t >= n_codes) break;
+    const int sblk = t >> 6, w = t & 63;
+    const int tx = (sblk % super_x) * 8 + morton3(w, 0);
+    const int ty = (sblk / super_x) * 8 + morton3(w, 1);
+    if (tx >= tiles_x || ty >= tiles_y) continue;
+    const int px = tx * 8 + (lane & 7), py = ty * 4 + (lane >> 3);
+    if (px >= a.camera.width || py >= a.camera.height) continue;
+
+    Ray r;
+    setup_ray(a, px, py, r);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t stations = 0;
+    // Stations whose gathers honour the guard form one interval (each cell
+    // index is monotone in k).  A bad first station is gathered by any hit
+    // ray: error.  A bad last station: binary-search the last good one and
+    // stop there; reaching that point without an iso hit / early stop is
+    // the reference's GuardContractError (fields.py:230-238).
+    long long kend = r.k_hi;
+    bool bad_tail = false;
+    if (r.hit && r.k_hi > r.k_lo) {  // a hit ray can hold no station (t_in, t_out in one step)
+      double pa[3], pb[3];
+      station_pos(o, r.d, dmul((double)r.k_lo, step), pa);
+      station_pos(o, r.d, dmul((double)(r.k_hi - 1), step), pb);
+      if (!cell_guard_ok(M, pa)) {
+        if (err) atomicAdd(err, 1u);
+        kend = r.k_lo;
+      } else if (!cell_guard_ok(M, pb)) {
+        long long good = r.k_lo, bad = r.k_hi - 1;
+        while (bad - good > 1) {
+          const long long mid = good + ((bad - good) >> 1);
+          double pm[3];
+          station_pos(o, r.d, dmul((double)mid, step), pm);
+          if (cell_guard_ok(M, pm)) good = mid;
+          else bad = mid;
+        }
+        kend = bad;
+        bad_tail = true;
+      }
+    }
+    if (r.hit) {
+      float prev[NS];
+#pragma unroll
+      for (int si = 0; si < NS; ++si) prev[si] = CUDART_NAN_F;
+      double kd = (double)r.k_lo;
+      const double kendd = (double)kend;
+      bool stopped = false;
+      for (; kd < kendd; kd = dadd(kd, 1.0)) {
+        ++stations;
+        double p[3];
+        station_pos(o, r.d, dmul(kd, step), p);
+        int ix, iy, iz;
+        float fx, fy, fz;
+        cell_of(p, ix, iy, iz, fx, fy, fz);
+        const int x0 = ix - M.lo[0], y0 = iy - M.lo[1], z0 = iz - M.lo[2];
+        float v[NS][4];
+        // all gathers of the station first (they are independent)
+        gather_guarded<dim_at<DIMS, 0>()>(M.s[0], x0, y0, z0, fx, fy, fz, v[0]);
+        if constexpr (NS > 1) gather_guarded<dim_at<DIMS, 1>()>(M.s[1], x0, y0, z0, fx, fy, fz, v[1]);
+        if constexpr (NS > 2) gather_guarded<dim_at<DIMS, 2>()>(M.s[2], x0, y0, z0, fx, fy, fz, v[2]);
+        if constexpr (NS > 3) gather_guarded<dim_at<DIMS, 3>()>(M.s[3], x0, y0, z0, fx, fy, fz, v[3]);
+        float4 st = make_float4(0.f, 0.f, 0.f, 0.f);
+        bool stop = false;
+#pragma unroll
+        for (int si = 0; si < NS; ++si) {
+          const isc_source& s = a.src[si];
+          const MultiSrc& S = M.s[si];
+          const int D = si == 0 ? dim_at<DIMS, 0>() : si == 1 ? dim_at<DIMS, 1>() : si == 2 ? dim_at<DIMS, 2>()
+                                                                                               : dim_at<DIMS, 3>();
+          const float cur = s.n_steps ? run_chain(s, v[si], D) : v[si][0];
+          const float4* lut = lut_s + si * ISC_LUT_ENTRIES;
+          const float inv = 1.0f / (s.range_hi - s.range_lo);
+          if (s.mode != ISC_ISO) {
+            st = over4(st, premultiply(classify(lut, s.range_lo, inv, cur)));
+            continue;
+          }
+          // ---- iso: raycast.py:384-468 (every source here is guarded: "exact") ----
+          const float thr = s.iso_threshold;
+          float before = prev[si];
+          const long long k = (long long)kd;
+          if (k == r.k_lo && k - 1 >= r.kg_lo) {  // entry pair: sample k-1 through the guard
+            double off[3], bsz[3], pq[3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+              off[i] = (double)a.brick_offset[i];
+              bsz[i] = (double)a.brick_size[i];
+            }
+            station_pos(o, r.d, dmul((double)(k - 1), step), pq);
+            before = reach(off, bsz, M.g, pq) ? point_scalar<true>(S, M, s, pq, err) : CUDART_NAN_F;
+          }
+          const float sa = before - thr, sb = cur - thr;
+          bool hit = isfinite(sa) && ((sa < 0.f) != (sb < 0.f));
+          double tau = 0.0, back = 0.0;
+          if (hit) {
+            const float den = sa - sb;
+            tau = den != 0.f ? (double)(sa / den) : 1.0;
+            back = -1.0;
+          }
+          if (!hit && k == r.k_hi - 1 && k + 1 < r.kg_hi) {  // exit pair, checked forward
+            double off[3], bsz[3], vb[3], pn[3], noff[3];
+            station_pos(o, r.d, dmul((double)(k + 1), step), pn);
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+              off[i] = (double)a.brick_offset[i];
+              bsz[i] = (double)a.brick_size[i];
+              vb[i] = ddiv((double)a.volume_size[i], (double)a.decomposition[i]);  // raycast.py:283-285
+              double c = floor(ddiv(pn[i], vb[i]));
+              c = dmin(dmax(c, 0.0), (double)(a.decomposition[i] - 1));
+              noff[i] = dmul(c, vb[i]);
+            }
+            if (reach(off, bsz, M.g, pn) && !reach(noff, vb, M.g, p)) {
+              const float sn = point_scalar<true>(S, M, s, pn, err) - thr;
+              if ((sb < 0.f) != (sn < 0.f)) {
+                const float den = sb - sn;
+                tau = den != 0.f ? (double)(sb / den) : 1.0;
+                back = 0.0;
+                hit = true;
+              }
+            }
+          }
+          prev[si] = cur;
+          if (hit) {
+            double hp[3], off[3];
+            int isz[3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+              off[i] = (double)a.brick_offset[i];
+              isz[i] = a.brick_size[i];
+            }
+            const double tt = dmul(dadd(tau, back), step);
+#pragma unroll
+            for (int i = 0; i < 3; ++i) hp[i] = dadd(p[i], dmul(tt, r.d[i]));
+            const float3 nrm = multi_normal<true>(S, M, s, off, isz, hp, r.d, err);
+            const float shade = fabsf(nrm.x * (float)r.d[0] + nrm.y * (float)r.d[1] + nrm.z * (float)r.d[2]);
+            const float4 base = classify(lut, s.range_lo, inv, thr);
+            st = over4(st, make_float4(base.x * shade, base.y * shade, base.z * shade, 1.0f));
+            stop = true;
+          }
+        }
+        acc = over4(acc, st);
+        if (stop || (gate_alpha && (double)acc.w >= a.alpha_stop)) {
+          stopped = true;
+          break;
+        }
+      }
+      if (bad_tail && !stopped && err) atomicAdd(err, 1u);
+    }
+    const long long pix = (long long)py * a.camera.width + px;
+    reinterpret_cast<float4*>(a.out_rgba)[pix] = acc;
+    warp_stations += stations;
+    if (a.out_stations) a.out_stations[pix] = stations;
+    if (a.out_hit) a.out_hit[pix] = r.hit ? 1 : 0;
+    if (a.out_t) {
+      a.out_t[2 * pix] = r.t_in;
+      a.out_t[2 * pix + 1] = r.t_out;
+    }
+    if (a.out_krange)
+      reinterpret_cast<int4*>(a.out_krange)[pix] = make_int4((int)r.k_lo, (int)r.k_hi, (int)r.kg_lo, (int)r.kg_hi);
+  }
+  if (a.out_station_total) {
+#pragma unroll
+    for (int off2 = 16; off2 > 0; off2 >>= 1) warp_stations += __shfl_xor_sync(0xffffffffu, warp_stations, off2);
+    if (lane == 0 && warp_stations) atomicAdd(a.out_station_total, warp_stations);
+  }
+}
+
+template <int NS, int DIMS>
+static int launch_multi_fast(const isc_render_args* a, const MultiField& M, cudaStream_t st) {
+  const int tiles_x = (a->camera.width + 7) / 8, tiles_y = (a->camera.height + 3) / 4;
+  const int super_x = (tiles_x + 7) / 8, super_y = (tiles_y + 7) / 8;
+  const int n_codes = super_x * super_y * 64;
+  int dev = 0, sms = 148, per_sm = 1;
+  ISC_CUDA_CHECK(cudaGetDevice(&dev));
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_multi_fast_kernel<NS, DIMS>, kThreads, 0);
+  int grid = sms * (per_sm > 0 ? per_sm : 1);
+  const int need = (n_codes + (kThreads / 32) - 1) / (kThreads / 32);
+  if (grid > need) grid = need > 0 ? need : 1;
+  march_multi_fast_kernel<NS, DIMS><<<grid, kThreads, 0, st>>>(*a, M, tiles_x, tiles_y, super_x, n_codes);
+  ISC_CUDA_CHECK(cudaGetLastError());
+  return ISC_OK;
+}
+
+// Dispatch of the specialised kernel: 1-2 sources of 1 or 3 components.
+static bool launch_multi_fast_dims(const isc_render_args* a, const MultiField& M, cudaStream_t st, int* status) {
+  const int ns = a->n_sources;
+  int dims = 0, scale = 1;
+  for (int si = 0; si < ns; ++si, scale *= 5) dims += a->src[si].feature_dim * scale;
+  switch (ns * 1000 + dims) {
+    case 1001: *status = launch_multi_fast<1, 1>(a, M, st); return true;
+    case 1003: *status = launch_multi_fast<1, 3>(a, M, st); return true;
+    case 2006: *status = launch_multi_fast<2, 1 + 5 * 1>(a, M, st); return true;
+    case 2016: *status = launch_multi_fast<2, 1 + 5 * 3>(a, M, st); return true;
+    case 2008: *status = launch_multi_fast<2, 3 + 5 * 1>(a, M, st); return true;
+    case 2018: *status = launch_multi_fast<2, 3 + 5 * 3>(a, M, st); return true;
+    default: return false;
+  }
+}
+
 template <int NS, bool INTERP, int MINB>
 static int launch_multi_m(const isc_render_args* a, const MultiField& M, cudaStream_t st) {
   const int tiles_x = (a->camera.width + 7) / 8, tiles_y = (a->camera.height + 3) / 4;
@@ -338,6 +606,10 @@ bool launch_multi(const isc_render_args* a, cudaStream_t st, int* status) {
     S.guarded = (s.has_guard && interp) ? 1 : 0;
     for (int i = 0; i < 3; ++i) S.hi[i] = S.guarded ? a->brick_size[i] + 2 * g - 2 : a->brick_size[i] - 1;
   }
+  static const bool no_multi_fast = getenv("ISC_DISABLE_MULTI_FAST") != nullptr;
+  bool all_guarded = interp;
+  for (int si = 0; si < ns; ++si) all_guarded = all_guarded && M.s[si].guarded;
+  if (!no_multi_fast && all_guarded && launch_multi_fast_dims(a, M, st, status)) return true;
   switch (ns * 2 + (interp ? 1 : 0)) {
     case 2: *status = launch_multi_t<1, false>(a, M, st); break;
     case 3: *status = launch_multi_t<1, true>(a, M, st); break;

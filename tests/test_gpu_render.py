@@ -163,6 +163,61 @@ def test_guard_contract_violation_raises():
         P.render_local(ctx, scene)
 
 
+@pytest.mark.parametrize("with_vector", [False, True])
+def test_guard_tail_reached_only_if_marched(with_vector):
+    """Guard contract on a brick whose far cells lack the halo (guard 0): rays
+    that stop at an iso surface before the far face gather no bad corner and
+    must not raise (the reference raises only on a gather it performs,
+    fields.py:230-238); the same rays in volume mode reach the far face and
+    must raise.  Covers the per-ray end-station proof of the specialised
+    kernels (march_multi.cu / march.cu)."""
+    import math
+    import paper_1611_09048_b200 as P
+    from oracle import isaac_oracle as O
+    torch = _torch()
+    n = 8
+    z, y, x = np.meshgrid(*(np.arange(n, dtype=np.float64),) * 3, indexing="ij")
+    scal = x.astype(np.float32)                        # iso at x = 2.5, reached from the x = 0 face
+    vec = np.stack([x, y, z], axis=-1).astype(np.float32) * 0.1
+    vol = P.GlobalVolume((n, n, n))
+    dom = vol.local_domain(0, 0)
+    cam = dict(position=(-50.0, 3.7, 3.3), look_at=(4.0, 3.7, 3.3), vertical_fov=math.radians(5.0),
+               width=16, height=12)
+    pts = [(0.0, 0.0, 0.0, 0.0, 0.0), (1.0, 1.0, 0.5, 0.2, 0.6)]
+
+    def render(mode):
+        reg = P.SourceRegistry(dom)
+        reg.register_handle(P.array_backed_handle(P.SourceDescriptor("s", 1, has_guard=True),
+                                                  torch.from_numpy(scal).cuda(), 0))
+        active = (0,)
+        if with_vector:
+            reg.register_handle(P.array_backed_handle(P.SourceDescriptor("v", 3, has_guard=True),
+                                                      torch.from_numpy(vec).cuda(), 0))
+            active = (0, 1)
+        P.update_sources(reg, set(active), {})
+        fr = P.default_registry()
+        scene = P.SceneState(
+            camera=P.Camera(cam["position"], cam["look_at"], vertical_fov=cam["vertical_fov"],
+                            image_size=(cam["width"], cam["height"])),
+            tf_points={i: pts for i in active}, value_ranges={i: (0.0, 8.0) for i in active},
+            chain_texts={0: "", 1: "length"} if with_vector else {0: ""},
+            settings=P.RenderSettings(active_set=active, modes={0: mode}, iso_thresholds={0: 2.5},
+                                      early_termination_alpha=1.0))
+        return P.render_local(P.RankContext(vol, dom, reg, fr, fr.limits), scene).pixels.cpu().numpy()
+
+    got = render("iso")
+    srcs = [O.Source(scal, (0, 0, 0), (n, n, n), 0, lut=O.lut_from_points(pts), value_range=(0.0, 8.0),
+                     mode="iso", iso_threshold=2.5)]
+    if with_vector:
+        srcs.append(O.Source(vec, (0, 0, 0), (n, n, n), 0, lut=O.lut_from_points(pts), value_range=(0.0, 8.0),
+                             steps=O.parse_steps("length", 3)))
+    ref = O.render_brick(cam, O.Brick((0, 0, 0), (n, n, n), 0, (n, n, n)), srcs)
+    assert (ref.rgba[..., 3] == 1.0).all()            # every ray stopped on the surface
+    assert np.abs(got - ref.rgba).max() <= 1e-3
+    with pytest.raises(P.GuardContractError):
+        render("volume")
+
+
 def test_value_range_bit_exact():
     import paper_1611_09048_b200 as P
     from oracle import isaac_oracle as O

@@ -296,3 +296,23 @@ def test_broadcast_scene_aborts_on_bad_chain_everywhere():
             return (ok == good, ctx.scene == good)
 
     assert P.run_ranks(3, body) == [(True, True)] * 3
+
+
+def test_station_cells_monotone_in_k():
+    """The kernels check the guard contract at a ray's end stations only; that
+    is exact because every axis of pos_k = o + (k*step)*d (float64,
+    round-to-nearest, raycast.py:346) is monotone in k, so each cell index
+    floor(pos_k) is too.  Checked on random rays, with positions evaluated
+    exactly as numpy (and the device) evaluate them."""
+    rng = np.random.default_rng(11)
+    k = np.arange(0, 4000, dtype=np.float64)
+    for _ in range(200):
+        o = rng.uniform(-3000.0, 3000.0, 3)
+        d = rng.normal(size=3)
+        d /= np.sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2])
+        step = float(rng.choice([0.5, 0.37, 1.0 / 3.0, 0.25]))
+        pos = o[None, :] + (k * step)[:, None] * d[None, :]
+        cells = np.floor(pos)
+        for a in range(3):
+            diff = np.diff(cells[:, a])
+            assert (diff >= 0).all() or (diff <= 0).all()
