@@ -351,6 +351,9 @@ __global__ void __launch_bounds__(kThreads, ISC_MULTI_FAST_MINB)
   const double step = a.step;
   uint32_t* err = a.error_word;
   unsigned long long warp_stations = 0;
+  float inv_span[NS];
+#pragma unroll
+  for (int si = 0; si < NS; ++si) inv_span[si] = 1.0f / (a.src[si].range_hi - a.src[si].range_lo);
 
   for (;;) {
     int t = 0;
@@ -422,11 +425,13 @@ __global__ void __launch_bounds__(kThreads, ISC_MULTI_FAST_MINB)
         for (int si = 0; si < NS; ++si) {
           const isc_source& s = a.src[si];
           const MultiSrc& S = M.s[si];
-          const int D = si == 0 ? dim_at<DIMS, 0>() : si == 1 ? dim_at<DIMS, 1>() : si == 2 ? dim_at<DIMS, 2>()
-                                                                                               : dim_at<DIMS, 3>();
-          const float cur = s.n_steps ? run_chain(s, v[si], D) : v[si][0];
+          float cur;
+          if (si == 0) cur = run_chain_fast<dim_at<DIMS, 0>()>(s, v[0]);
+          else if (si == 1) cur = run_chain_fast<dim_at<DIMS, 1>()>(s, v[1]);
+          else if (si == 2) cur = run_chain_fast<dim_at<DIMS, 2>()>(s, v[2]);
+          else cur = run_chain_fast<dim_at<DIMS, 3>()>(s, v[3]);
           const float4* lut = lut_s + si * ISC_LUT_ENTRIES;
-          const float inv = 1.0f / (s.range_hi - s.range_lo);
+          const float inv = inv_span[si];
           if (s.mode != ISC_ISO) {
             st = over4(st, premultiply(classify(lut, s.range_lo, inv, cur)));
             continue;

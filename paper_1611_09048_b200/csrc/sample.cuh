@@ -166,6 +166,53 @@ __device__ __forceinline__ float run_chain(const isc_source& s, float v[4], int 
   return v[0];
 }
 
+// One dimension-preserving chain step other than add / mul (pow, sqrt, abs,
+// neg, exp, log, min, max): out of line, the kernels' hot loops only carry
+// the common steps.
+static __device__ __noinline__ void chain_step_rare(const isc_chain_step& st, float* v, int dim) {
+  isc_source one{};
+  one.n_steps = 1;
+  one.steps[0] = st;
+  float w[4] = {v[0], v[1], v[2], v[3]};
+  run_chain(one, w, dim);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) v[c] = w[c];
+}
+
+// run_chain for a source whose input has D components (compile time): the
+// common steps (add, mul, length, sum) are tested first with uniform
+// branches and no per-component dimension tests; results are identical to
+// run_chain (same float32 operations in the same order).  After a reducing
+// step only component 0 is meaningful; the others keep being computed and are
+// ignored.
+template <int D>
+__device__ __forceinline__ float run_chain_fast(const isc_source& s, float v[4]) {
+  bool reduced = (D == 1);
+  for (int i = 0; i < s.n_steps; ++i) {
+    const isc_chain_step& st = s.steps[i];
+    const int op = st.op;
+    if (op == ISC_OP_ADD) {
+#pragma unroll
+      for (int c = 0; c < D; ++c) v[c] = fadd(v[c], st.arg[c]);
+    } else if (op == ISC_OP_MUL) {
+#pragma unroll
+      for (int c = 0; c < D; ++c) v[c] = fmul(v[c], st.arg[c]);
+    } else if (op == ISC_OP_LENGTH || op == ISC_OP_SUM) {
+      const bool len = op == ISC_OP_LENGTH;
+      float acc = len ? fmul(v[0], v[0]) : v[0];
+      if (!reduced) {
+#pragma unroll
+        for (int c = 1; c < D; ++c) acc = fadd(acc, len ? fmul(v[c], v[c]) : v[c]);
+      }
+      v[0] = len ? __fsqrt_rn(acc) : acc;
+      reduced = true;
+    } else {
+      chain_step_rare(st, v, reduced ? 1 : D);
+    }
+  }
+  return v[0];
+}
+
 // Straight RGBA from a LUT held in shared memory.
 __device__ __forceinline__ float4 classify(const float4* lut, float lo, float inv_span, float v) {
   if (!isfinite(v)) return make_float4(0.f, 0.f, 0.f, 0.f);
