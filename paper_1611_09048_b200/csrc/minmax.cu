@@ -3,7 +3,7 @@
 // function for this (value ranges are scene state, scene.py:188,
 // runtime.py:154-157); it feeds the auto value range of a transfer function.
 //
-// Streaming reduction: each warp walks whole x-rows (coalesced loads, 4
+// Streaming reduction: each warp walks whole x-rows (coalesced loads, 16
 // loads per lane in flight for memory-level parallelism), reduces with warp
 // shuffles, then one shared-memory pass per CTA and one ordered-integer
 // atomicMin/atomicMax per CTA.  min/max are exact, so the result is
@@ -19,6 +19,22 @@ __device__ __forceinline__ unsigned int order_key(float f) {
 }
 __device__ __forceinline__ float from_key(unsigned int k) {
   return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+#ifndef ISC_MINMAX_UNROLL
+#define ISC_MINMAX_UNROLL 16
+#endif
+constexpr int kUnroll = ISC_MINMAX_UNROLL;
+
+// Streaming read (each element is read once): evict-first.
+template <bool F32>
+__device__ __forceinline__ float load_stream(const isc_source& s, long long idx) {
+#ifdef ISC_MINMAX_LDG
+  return load_as<F32>(s, idx);
+#else
+  if constexpr (F32) return __ldcs(reinterpret_cast<const float*>(s.data) + idx);
+  else return load_elem(s, idx);
+#endif
 }
 
 __global__ void minmax_init(unsigned int* keys) {
@@ -45,24 +61,24 @@ __global__ void __launch_bounds__(256) minmax_kernel(const __grid_constant__ isc
   for (long long row = warp; row < rows; row += nwarps) {
     const int y = (int)(row % sy), z = (int)(row / sy);
     const long long base = (long long)(z + g) * s.stride[0] + (long long)(y + g) * s.stride[1] + (long long)g * s.stride[2];
-    // 4 independent loads per lane in flight (memory-level parallelism)
+    // kUnroll independent loads per lane in flight (memory-level parallelism)
     int x = lane;
-    for (; x + 96 < sx; x += 128) {
-      float v[4][4];
+    for (; x + 32 * (kUnroll - 1) < sx; x += 32 * kUnroll) {
+      float v[kUnroll][4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kUnroll; ++u) {
         const long long e = base + (long long)(x + 32 * u) * s.stride[2];
 #pragma unroll
-        for (int c = 0; c < DIM; ++c) v[u][c] = load_as<F32>(s, e + c * s.stride[3]);
+        for (int c = 0; c < DIM; ++c) v[u][c] = load_stream<F32>(s, e + c * s.stride[3]);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) visit(run_chain(s, v[u], DIM));
+      for (int u = 0; u < kUnroll; ++u) visit(run_chain(s, v[u], DIM));
     }
     for (; x < sx; x += 32) {
       const long long e = base + (long long)x * s.stride[2];
       float v[4];
 #pragma unroll
-      for (int c = 0; c < DIM; ++c) v[c] = load_as<F32>(s, e + c * s.stride[3]);
+      for (int c = 0; c < DIM; ++c) v[c] = load_stream<F32>(s, e + c * s.stride[3]);
       visit(run_chain(s, v, DIM));
     }
   }
