@@ -242,7 +242,7 @@ __device__ __forceinline__ float4 classify_line_premul(const isc_source& s, floa
 #ifndef ISC_FAST_MINB
 #define ISC_FAST_MINB 4  // <= 64 registers: 4 CTAs (32 warps) per SM
 #endif
-template <bool INTERP, bool GUARDED, bool PAIRED, bool LINE = false>
+template <bool INTERP, bool GUARDED, bool PAIRED, bool LINE = false, int DIM = 1>
 __global__ void __launch_bounds__(kThreads, ISC_FAST_MINB) march_fast_kernel(const __grid_constant__ isc_render_args a,
                                                               const FastField F, int tiles_x, int tiles_y,
                                                               int super_x, int n_codes, int row_order,
@@ -332,9 +332,17 @@ __global__ void __launch_bounds__(kThreads, ISC_FAST_MINB) march_fast_kernel(con
         if (left > 0) {
           double p0[3];
           station_pos(o, r.d, dmul(kd, step), p0);
-          const float v0 = fast_sample<INTERP, GUARDED, kCheck>(F, p0, err);
-          float vv[4] = {v0, 0.f, 0.f, 0.f};
-          const float s0 = s.n_steps ? run_chain(s, vv, 1) : v0;
+          float s0;
+          if constexpr (DIM == 1) {
+            const float v0 = fast_sample<INTERP, GUARDED, kCheck>(F, p0, err);
+            float vv[4] = {v0, 0.f, 0.f, 0.f};
+            s0 = s.n_steps ? run_chain(s, vv, 1) : v0;
+          } else {
+            static_assert(INTERP && GUARDED && PAIRED, "vector sources: guarded trilinear paired path only");
+            float vv[4] = {0.f, 0.f, 0.f, 0.f};
+            fast_gather<DIM>(F, p0, vv);
+            s0 = run_chain_fast<DIM>(s, vv);
+          }
           c = LINE ? classify_line_premul(s, lo, inv, s0) : premultiply(classify(lut_s, lo, inv, s0));
         }
         // Only the even lane's accumulator is used (it writes the pixel), so
@@ -452,7 +460,9 @@ using namespace isc;
 static bool fast_eligible(const isc_render_args* a, FastField& F) {
   if (a->n_sources != 1 || !a->work_counter) return false;
   const isc_source& s = a->src[0];
-  if (s.feature_dim != 1 || s.mode != ISC_VOLUME || s.dtype != ISC_F32) return false;
+  if ((s.feature_dim != 1 && s.feature_dim != 3) || s.mode != ISC_VOLUME || s.dtype != ISC_F32) return false;
+  // vector sources: guarded trilinear without early termination (paired path)
+  if (s.feature_dim == 3 && !(a->interpolation && s.has_guard && a->alpha_stop >= 1.0)) return false;
   const int g = a->guard_width;
   long long ext[3];
   for (int i = 0; i < 3; ++i) ext[i] = a->brick_size[i] + 2LL * g;
@@ -462,11 +472,14 @@ static bool fast_eligible(const isc_render_args* a, FastField& F) {
     if (s.stride[i] < 0 || s.stride[i] > INT32_MAX) return false;
     maxoff += (ext[2 - i] - 1) * s.stride[i];
   }
+  if (s.stride[3] < 0 || s.stride[3] > INT32_MAX) return false;
+  maxoff += (s.feature_dim - 1) * s.stride[3];
   if (maxoff + s.stride[0] + s.stride[1] + s.stride[2] >= INT32_MAX) return false;
   F.f = reinterpret_cast<const float*>(s.data);
   F.sz = (int)s.stride[0];
   F.sy = (int)s.stride[1];
   F.sx = (int)s.stride[2];
+  F.sc = (int)s.stride[3];
   F.g = g;
   const bool guarded = s.has_guard && a->interpolation;
   for (int i = 0; i < 3; ++i) {
@@ -476,7 +489,7 @@ static bool fast_eligible(const isc_render_args* a, FastField& F) {
   return true;
 }
 
-template <bool INTERP, bool GUARDED, bool PAIRED, bool LINE = false>
+template <bool INTERP, bool GUARDED, bool PAIRED, bool LINE = false, int DIM = 1>
 static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_t st) {
   static const int tw_log2 = getenv("ISC_TILE_W") ? __builtin_ctz(atoi(getenv("ISC_TILE_W"))) : 3;
   const int tw = 1 << tw_log2, th = (PAIRED ? 16 : 32) >> tw_log2;
@@ -487,12 +500,12 @@ static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_
   int dev = 0, sms = 148, per_sm = 1;
   ISC_CUDA_CHECK(cudaGetDevice(&dev));
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_fast_kernel<INTERP, GUARDED, PAIRED, LINE>, kThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_fast_kernel<INTERP, GUARDED, PAIRED, LINE, DIM>, kThreads, 0);
   const int total_warps = (n_codes + 0);
   int grid = sms * (per_sm > 0 ? per_sm : 1);
   const int need = (total_warps + (kThreads / 32) - 1) / (kThreads / 32);
   if (grid > need) grid = need > 0 ? need : 1;
-  march_fast_kernel<INTERP, GUARDED, PAIRED, LINE><<<grid, kThreads, 0, st>>>(*a, F, tiles_x, tiles_y, super_x, n_codes, row_order ? 1 : 0,
+  march_fast_kernel<INTERP, GUARDED, PAIRED, LINE, DIM><<<grid, kThreads, 0, st>>>(*a, F, tiles_x, tiles_y, super_x, n_codes, row_order ? 1 : 0,
                                                                  tw_log2);
   ISC_CUDA_CHECK(cudaGetLastError());
   return ISC_OK;
@@ -512,6 +525,9 @@ extern "C" int isc_render_local(const isc_render_args* a, void* stream) {
     const bool guarded = interp && a->src[0].has_guard;
     static const bool no_pair = getenv("ISC_DISABLE_PAIRED") != nullptr;
     const bool paired = !no_pair && a->alpha_stop >= 1.0;
+    if (a->src[0].feature_dim == 3)
+      return a->src[0].lut_linear ? launch_fast<true, true, true, true, 3>(a, F, s)
+                                  : launch_fast<true, true, true, false, 3>(a, F, s);
     if (interp && guarded && paired && a->src[0].lut_linear) return launch_fast<true, true, true, true>(a, F, s);
     if (interp && guarded) return paired ? launch_fast<true, true, true>(a, F, s) : launch_fast<true, true, false>(a, F, s);
     if (interp) return paired ? launch_fast<true, false, true>(a, F, s) : launch_fast<true, false, false>(a, F, s);

@@ -14,6 +14,7 @@ constexpr int kThreads = kTile * kTile;
 struct FastField {
   const float* __restrict__ f;
   int sx, sy, sz;        // element strides
+  int sc;                // component stride (feature_dim > 1)
   int lo[3];             // brick offset - guard (global cell of array index 0)
   int hi[3];             // largest legal base index (guarded) / size-1 (clamped)
   int g;
@@ -90,6 +91,29 @@ __device__ __forceinline__ float fast_sample(const FastField& F, const double p[
     const float a2 = fmaf(fx, v101 - v001, v001), a3 = fmaf(fx, v111 - v011, v011);
     const float b0 = fmaf(fy, a1 - a0, a0), b1 = fmaf(fy, a3 - a2, a2);
     return fmaf(fz, b1 - b0, b0);
+  }
+}
+
+// DIM-component trilinear gather with the guard contract already proven for
+// this station (march_fast_kernel's per-ray check): v[c] for c < DIM.
+template <int DIM>
+__device__ __forceinline__ void fast_gather(const FastField& F, const double p[3], float v[4]) {
+  int ix, iy, iz;
+  const double flx = floor_split(p[0], ix), fly = floor_split(p[1], iy), flz = floor_split(p[2], iz);
+  const float fx = (float)dsub(p[0], flx), fy = (float)dsub(p[1], fly), fz = (float)dsub(p[2], flz);
+  const int x0 = ix - F.lo[0], y0 = iy - F.lo[1], z0 = iz - F.lo[2];
+  const float* b = F.f + (z0 * F.sz + y0 * F.sy + x0 * F.sx);
+  const int dx = F.sx, dy = F.sy, dz = F.sz;
+#pragma unroll
+  for (int c = 0; c < DIM; ++c) {
+    const float* q0 = b + c * F.sc;
+    const float v000 = __ldg(q0), v100 = __ldg(q0 + dx), v010 = __ldg(q0 + dy), v110 = __ldg(q0 + dy + dx);
+    const float* q1 = q0 + dz;
+    const float v001 = __ldg(q1), v101 = __ldg(q1 + dx), v011 = __ldg(q1 + dy), v111 = __ldg(q1 + dy + dx);
+    const float a0 = fmaf(fx, v100 - v000, v000), a1 = fmaf(fx, v110 - v010, v010);
+    const float a2 = fmaf(fx, v101 - v001, v001), a3 = fmaf(fx, v111 - v011, v011);
+    const float b0 = fmaf(fy, a1 - a0, a0), b1 = fmaf(fy, a3 - a2, a2);
+    v[c] = fmaf(fz, b1 - b0, b0);
   }
 }
 

@@ -81,6 +81,15 @@ RENDER_CASES = {
                           sources=[src("random_vec3", chain="sum", rng=(0.0, 3.0), tf=WARM_TF),
                                    src("sphere_c", rng=(0.0, 24.0), tf=COOL_TF, mode="iso", iso=20.0)],
                           active=[0, 1]),
+    # single float3 source in volume mode (the paired vector march): LUT and
+    # analytic (single-ramp) classification
+    "vec_volume": dict(size=[24, 24, 24], decompositions=[[1, 1, 1], [2, 1, 1]],
+                       camera=harness_camera(24, (48, 32)),
+                       sources=[src("vector", chain="length | mul(2) | add(0.1)", rng=(0.0, 3.0), tf=COOL_TF)],
+                       active=[0]),
+    "vec_linear": dict(size=[20, 20, 20], decompositions=[[1, 1, 1], [1, 2, 1]],
+                       camera=test_camera(20, (40, 30)),
+                       sources=[src("random_vec3", chain="sum", rng=(0.0, 3.0))], active=[0]),
 }
 
 DEFAULTS = dict(step=0.5, alpha_stop=1.0, interp=True, planes=[], guard=1)

@@ -1,7 +1,8 @@
 """Generate golden vectors by running the REAL reference (``/root/reference``).
 
 Run in the build container only (the reference does not exist on the GPU
-box):  ``python tests/golden/make_golden.py``.  Outputs ``tests/golden/*.npz``
+box):  ``python tests/golden/make_golden.py`` (all) or
+``python tests/golden/make_golden.py --only name,name`` (render cases).  Outputs ``tests/golden/*.npz``
 plus ``manifest.json``; those files are committed and are what the tests read.
 
 Every array here comes out of the reference's own public or module-level
@@ -238,6 +239,17 @@ def toy_goldens():
 
 
 def main():
+    if len(sys.argv) > 2 and sys.argv[1] == "--only":
+        # regenerate the named render cases only (manifest entries updated in place)
+        with open(os.path.join(HERE, "manifest.json")) as fh:
+            manifest = json.load(fh)
+        for name in sys.argv[2].split(","):
+            np.savez_compressed(os.path.join(HERE, f"render_{name}.npz"), **render_case(name))
+            manifest["render"][name] = f"render_{name}.npz"
+        with open(os.path.join(HERE, "manifest.json"), "w") as fh:
+            json.dump(manifest, fh, indent=1)
+        print("done")
+        return
     manifest = {"reference": "/root/reference/pkg/src/insitu (insitu 0.1.0)",
                 "numpy": np.__version__, "render": {}, "composite": {}}
     print("render cases:")
