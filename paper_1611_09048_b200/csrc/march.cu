@@ -20,8 +20,6 @@
 namespace isc {
 
 bool launch_multi(const isc_render_args* a, cudaStream_t st, int* status);  // march_multi.cu
-bool launch_iso_probe(const isc_render_args* a, cudaStream_t st, int* kend_px, float4* tail_px, int incl,
-                      int* status);  // march_multi.cu
 
 __device__ __forceinline__ void tile_pixel(int& px, int& py) {
   const int t = threadIdx.x, w = t >> 5, l = t & 31;
@@ -248,8 +246,7 @@ template <bool INTERP, bool GUARDED, bool PAIRED, bool LINE = false, int DIM = 1
 __global__ void __launch_bounds__(kThreads, ISC_FAST_MINB) march_fast_kernel(const __grid_constant__ isc_render_args a,
                                                               const FastField F, int tiles_x, int tiles_y,
                                                               int super_x, int n_codes, int row_order,
-                                                              int tw_log2, const int* __restrict__ kend_px,
-                                                              const float4* __restrict__ tail_px) {
+                                                              int tw_log2) {
   __shared__ float4 lut_s[ISC_LUT_ENTRIES];
   for (int i = threadIdx.x; i < ISC_LUT_ENTRIES; i += blockDim.x)
     lut_s[i] = reinterpret_cast<const float4*>(a.src[0].lut)[i];
@@ -301,10 +298,8 @@ __global__ void __launch_bounds__(kThreads, ISC_FAST_MINB) march_fast_kernel(con
       // the full mask (a per-lane mask costs a MATCH.ANY convergence check per
       // shuffle).  Lanes whose ray is finished contribute transparent samples:
       // over(acc, 0) == acc exactly.
-      // pass 2 of the iso + volume split: stop where the iso probe ended
-      const long long k_hi = (kend_px && in_img) ? min(r.k_hi, (long long)kend_px[(long long)py * a.camera.width + px])
-                                                 : r.k_hi;
-      const long long n = (r.hit && k_hi > r.k_lo) ? (k_hi - r.k_lo) : 0;
+      const long long k_hi = r.k_hi;
+      const long long n = r.hit ? (k_hi - r.k_lo) : 0;
       long long nm = n;  // stations this lane pair marches
 #ifndef ISC_EXP_SAMPLE_GUARD
       // Guard contract checked once per ray: every axis of the station
@@ -362,7 +357,6 @@ __global__ void __launch_bounds__(kThreads, ISC_FAST_MINB) march_fast_kernel(con
         warp_stations += stations;
         continue;
       }
-      if (tail_px) acc = over4(acc, tail_px[(long long)py * a.camera.width + px]);
     } else if (r.hit) {
       long long k = r.k_lo;
       if (!gate_alpha) {
@@ -497,8 +491,7 @@ static bool fast_eligible(const isc_render_args* a, FastField& F) {
 }
 
 template <bool INTERP, bool GUARDED, bool PAIRED, bool LINE = false, int DIM = 1>
-static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_t st,
-                       const int* kend_px = nullptr, const float4* tail_px = nullptr) {
+static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_t st) {
   static const int tw_log2 = getenv("ISC_TILE_W") ? __builtin_ctz(atoi(getenv("ISC_TILE_W"))) : 3;
   const int tw = 1 << tw_log2, th = (PAIRED ? 16 : 32) >> tw_log2;
   const int tiles_x = (a->camera.width + tw - 1) / tw, tiles_y = (a->camera.height + th - 1) / th;
@@ -514,82 +507,9 @@ static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_
   const int need = (total_warps + (kThreads / 32) - 1) / (kThreads / 32);
   if (grid > need) grid = need > 0 ? need : 1;
   march_fast_kernel<INTERP, GUARDED, PAIRED, LINE, DIM><<<grid, kThreads, 0, st>>>(
-      *a, F, tiles_x, tiles_y, super_x, n_codes, row_order ? 1 : 0, tw_log2, kend_px, tail_px);
+      *a, F, tiles_x, tiles_y, super_x, n_codes, row_order ? 1 : 0, tw_log2);
   ISC_CUDA_CHECK(cudaGetLastError());
   return ISC_OK;
-}
-
-// Iso + volume split (the C3 shape: one iso source, one volume source, no
-// early termination, guarded trilinear float32).  The iso surface is opaque,
-// so the combined per-station loop of raycast.march_rays (raycast.py:349-380)
-// factors exactly into
-//   pass 1  march the iso source alone (march_multi_fast_kernel PROBE): per
-//           pixel the hit station k* and the shaded iso colour; station
-//           counts, hit mask and ranges are written here (the combined loop
-//           stops at k* too);
-//   pass 2  march the volume source with the paired kernel over
-//           [k_lo, k*) -- or [k_lo, k*] when the volume source precedes the
-//           iso source in source-id order, since its sample at k* is then
-//           composited in front of the opaque iso colour -- and composite
-//           the iso colour last.
-// Scratch (int k_end + float4 colour per pixel) is stream-ordered.
-static bool split_eligible(const isc_render_args* a, int& iso, int& vol) {
-  if (a->n_sources != 2 || !a->work_counter || a->alpha_stop < 1.0 || !a->interpolation) return false;
-  const int m0 = a->src[0].mode, m1 = a->src[1].mode;
-  if (m0 == m1) return false;
-  iso = m0 == ISC_ISO ? 0 : 1;
-  vol = 1 - iso;
-  const isc_source& si = a->src[iso];
-  if (!si.has_guard || si.dtype != ISC_F32 || (si.feature_dim != 1 && si.feature_dim != 3)) return false;
-  return true;
-}
-
-static int render_split(const isc_render_args* a, int iso, int vol, const FastField& F, cudaStream_t s, bool* done) {
-  *done = false;
-  const long long npx = (long long)a->camera.width * a->camera.height;
-  static bool pool_ready = false;
-  if (!pool_ready) {  // keep freed scratch in the pool between frames
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t keep = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-    pool_ready = true;
-  }
-  void* scratch = nullptr;
-  ISC_CUDA_CHECK(cudaMallocAsync(&scratch, (size_t)npx * (sizeof(float4) + sizeof(int)), s));
-  float4* tail = reinterpret_cast<float4*>(scratch);
-  int* kend = reinterpret_cast<int*>(tail + npx);
-  isc_render_args a1 = *a;
-  a1.n_sources = 1;
-  a1.src[0] = a->src[iso];
-  int status = ISC_OK;
-  if (!launch_iso_probe(&a1, s, kend, tail, vol < iso ? 1 : 0, &status)) {
-    cudaFreeAsync(scratch, s);
-    return ISC_OK;  // not handled: caller falls through
-  }
-  if (status == ISC_OK) {
-    isc_render_args a2 = *a;
-    a2.n_sources = 1;
-    a2.src[0] = a->src[vol];
-    a2.out_stations = nullptr;
-    a2.out_station_total = nullptr;
-    a2.out_hit = nullptr;
-    a2.out_t = nullptr;
-    a2.out_krange = nullptr;
-    cudaError_t e = cudaMemsetAsync(a2.work_counter, 0, sizeof(uint32_t), s);
-    if (e != cudaSuccess) status = cuda_fail(e, "cudaMemsetAsync");
-    else if (a2.src[0].feature_dim == 3)
-      status = a2.src[0].lut_linear ? launch_fast<true, true, true, true, 3>(&a2, F, s, kend, tail)
-                                    : launch_fast<true, true, true, false, 3>(&a2, F, s, kend, tail);
-    else
-      status = a2.src[0].lut_linear ? launch_fast<true, true, true, true>(&a2, F, s, kend, tail)
-                                    : launch_fast<true, true, true>(&a2, F, s, kend, tail);
-  }
-  cudaFreeAsync(scratch, s);
-  *done = true;
-  return status;
 }
 
 extern "C" int isc_render_local(const isc_render_args* a, void* stream) {
@@ -599,20 +519,6 @@ extern "C" int isc_render_local(const isc_render_args* a, void* stream) {
   if (a->error_word) ISC_CUDA_CHECK(cudaMemsetAsync(a->error_word, 0, sizeof(uint32_t), s));
   if (a->out_station_total) ISC_CUDA_CHECK(cudaMemsetAsync(a->out_station_total, 0, sizeof(unsigned long long), s));
   if (a->work_counter) ISC_CUDA_CHECK(cudaMemsetAsync(a->work_counter, 0, sizeof(uint32_t), s));
-  static const bool no_split = getenv("ISC_DISABLE_SPLIT") != nullptr;
-  int iso_i = 0, vol_i = 0;
-  if (!no_split && split_eligible(a, iso_i, vol_i)) {
-    // the volume source must take the paired fast path
-    isc_render_args av = *a;
-    av.n_sources = 1;
-    av.src[0] = a->src[vol_i];
-    FastField FV;
-    if (fast_eligible(&av, FV) && av.src[0].has_guard) {
-      bool done = false;
-      const int rs = render_split(a, iso_i, vol_i, FV, s, &done);
-      if (done) return rs;
-    }
-  }
   FastField F;
   static const bool no_fast = getenv("ISC_DISABLE_FAST") != nullptr;
   if (!no_fast && fast_eligible(a, F)) {

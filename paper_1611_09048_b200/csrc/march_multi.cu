@@ -333,6 +333,31 @@ __device__ __forceinline__ bool cell_guard_ok(const MultiField& M, const double 
          (unsigned)(iz - M.lo[2]) <= (unsigned)S.hi[2];
 }
 
+// Shaded colour of an iso hit on source si (gradient normal, raycast.py:
+// 210-242, 351-369), out of line so the station loop keeps its registers;
+// direction and position by value so the caller's Ray stays in registers.
+__device__ __noinline__ float4 iso_hit_color(const isc_render_args& a, const MultiField& M, int si, double d0,
+                                             double d1, double d2, double p0, double p1, double p2, double tau,
+                                             double back, uint32_t* err) {
+  const double d[3] = {d0, d1, d2}, p[3] = {p0, p1, p2};
+  const isc_source& s = a.src[si];
+  double hp[3], off[3];
+  int isz[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    off[i] = (double)a.brick_offset[i];
+    isz[i] = a.brick_size[i];
+  }
+  const double tt = dmul(dadd(tau, back), a.step);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) hp[i] = dadd(p[i], dmul(tt, d[i]));
+  const float3 nrm = multi_normal<true>(M.s[si], M, s, off, isz, hp, d, err);
+  const float shade = fabsf(nrm.x * (float)d[0] + nrm.y * (float)d[1] + nrm.z * (float)d[2]);
+  const float4 base = classify(reinterpret_cast<const float4*>(s.lut), s.range_lo, 1.0f / (s.range_hi - s.range_lo),
+                               s.iso_threshold);
+  return make_float4(base.x * shade, base.y * shade, base.z * shade, 1.0f);
+}
+
 #ifndef ISC_MULTI_FAST_MINB
 #define ISC_MULTI_FAST_MINB 2
 #endif
@@ -400,6 +425,10 @@ __global__ void __launch_bounds__(kThreads, ISC_MULTI_FAST_MINB)
       }
     }
     bool stopped = false;
+    int hit_si = -1;                     // first iso source hit (shaded after the loop)
+    long long hit_k = 0;
+    double hit_tau = 0.0, hit_back = 0.0;
+    float4 hit_front = make_float4(0.f, 0.f, 0.f, 0.f);  // the station's sources in front of it
     if (r.hit) {
       float prev[NS];
 #pragma unroll
@@ -482,32 +511,35 @@ __global__ void __launch_bounds__(kThreads, ISC_MULTI_FAST_MINB)
             }
           }
           prev[si] = cur;
-          if (hit) {
-            double hp[3], off[3];
-            int isz[3];
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {
-              off[i] = (double)a.brick_offset[i];
-              isz[i] = a.brick_size[i];
-            }
-            const double tt = dmul(dadd(tau, back), step);
-#pragma unroll
-            for (int i = 0; i < 3; ++i) hp[i] = dadd(p[i], dmul(tt, r.d[i]));
-            const double dd[3] = {r.d[0], r.d[1], r.d[2]};  // keeps the Ray out of local memory
-            const float3 nrm = multi_normal<true>(S, M, s, off, isz, hp, dd, err);
-            const float shade = fabsf(nrm.x * (float)r.d[0] + nrm.y * (float)r.d[1] + nrm.z * (float)r.d[2]);
-            const float4 base = classify(lut, s.range_lo, inv, thr);
-            st = over4(st, make_float4(base.x * shade, base.y * shade, base.z * shade, 1.0f));
+          if (hit && !stop) {  // later sources of the station sit behind the opaque hit
+            hit_si = si;
+            hit_k = k;
+            hit_tau = tau;
+            hit_back = back;
+            hit_front = st;
             stop = true;
           }
         }
+        if (stop) {
+          stopped = true;
+          break;
+        }
         acc = over4(acc, st);
-        if (stop || (gate_alpha && (double)acc.w >= a.alpha_stop)) {
+        if (gate_alpha && (double)acc.w >= a.alpha_stop) {
           stopped = true;
           break;
         }
       }
       if (bad_tail && !stopped && err) atomicAdd(err, 1u);
+    }
+    // Shade iso hits after the loop: hits fall in different iterations, so
+    // in-loop shading ran once per hitting lane with the rest of the warp idle.
+    if (hit_si >= 0) {
+      double ph[3];
+      station_pos(o, r.d, dmul((double)hit_k, step), ph);
+      const float4 c = iso_hit_color(a, M, hit_si, r.d[0], r.d[1], r.d[2], ph[0], ph[1], ph[2], hit_tau, hit_back,
+                                     err);
+      acc = over4(acc, over4(hit_front, c));
     }
     const long long pix = (long long)py * a.camera.width + px;
     reinterpret_cast<float4*>(a.out_rgba)[pix] = acc;
@@ -584,267 +616,7 @@ static int launch_multi_t(const isc_render_args* a, const MultiField& M, cudaStr
   return launch_multi_m<NS, INTERP, 2>(a, M, st);
 }
 
-// ---------------------------------------------------------------------------
-// Paired iso probe (pass 1 of the iso + volume split, march.cu): one guarded
-// trilinear iso source of DIM components.  A warp is 16 rays (8x2 pixels) x 2
-// station parities as in march_fast_kernel; lane l + 16 marches the odd
-// stations of lane l's ray.  The sign test of station k needs station k-1:
-// the odd lane takes it from its even partner in the same iteration, the
-// even lane from the odd partner's previous iteration (both by shuffle).
-// Entry pairs (k_lo - 1 through the guard), forward exit pairs and the
-// gradient shading are the reference's (raycast.py:384-468, 210-242, 351-369)
-// on the lane holding the station; the even station wins a pair.  Output per
-// pixel: the exclusive end of the companion volume march and the iso colour.
-#ifndef ISC_PROBE_MINB
-#define ISC_PROBE_MINB 4
-#endif
-// Rare paths of the paired iso probe, out of line so the station loop keeps
-// its registers: the entry-pair value (station k_lo - 1 through the guard),
-// the forward exit pair, and the shaded colour of a hit.
-__device__ __noinline__ float iso_entry_value(const isc_render_args& a, const MultiField& M, double d0, double d1,
-                                              double d2, long long k, uint32_t* err) {
-  const double d[3] = {d0, d1, d2};
-  double off[3], bsz[3], pq[3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    off[i] = (double)a.brick_offset[i];
-    bsz[i] = (double)a.brick_size[i];
-  }
-  station_pos(a.camera.origin, d, dmul((double)(k - 1), a.step), pq);
-  return reach(off, bsz, M.g, pq) ? point_scalar<true>(M.s[0], M, a.src[0], pq, err) : CUDART_NAN_F;
-}
-
-__device__ __noinline__ bool iso_exit_pair(const isc_render_args& a, const MultiField& M, double d0, double d1,
-                                           double d2, long long k, double p0, double p1, double p2, float sb,
-                                           double* tau, uint32_t* err) {
-  const double d[3] = {d0, d1, d2}, p[3] = {p0, p1, p2};
-  double off[3], bsz[3], vb[3], pn[3], noff[3];
-  station_pos(a.camera.origin, d, dmul((double)(k + 1), a.step), pn);
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    off[i] = (double)a.brick_offset[i];
-    bsz[i] = (double)a.brick_size[i];
-    vb[i] = ddiv((double)a.volume_size[i], (double)a.decomposition[i]);  // raycast.py:283-285
-    double c = floor(ddiv(pn[i], vb[i]));
-    c = dmin(dmax(c, 0.0), (double)(a.decomposition[i] - 1));
-    noff[i] = dmul(c, vb[i]);
-  }
-  if (reach(off, bsz, M.g, pn) && !reach(noff, vb, M.g, p)) {
-    const float sn = point_scalar<true>(M.s[0], M, a.src[0], pn, err) - a.src[0].iso_threshold;
-    if ((sb < 0.f) != (sn < 0.f)) {
-      const float den = sb - sn;
-      *tau = den != 0.f ? (double)(sb / den) : 1.0;
-      return true;
-    }
-  }
-  return false;
-}
-
-__device__ __noinline__ float4 iso_hit_color(const isc_render_args& a, const MultiField& M, double d0, double d1,
-                                             double d2, double p0, double p1, double p2, double tau, double back,
-                                             uint32_t* err) {
-  const double d[3] = {d0, d1, d2}, p[3] = {p0, p1, p2};
-  const isc_source& s = a.src[0];
-  double hp[3], off[3];
-  int isz[3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    off[i] = (double)a.brick_offset[i];
-    isz[i] = a.brick_size[i];
-  }
-  const double tt = dmul(dadd(tau, back), a.step);
-#pragma unroll
-  for (int i = 0; i < 3; ++i) hp[i] = dadd(p[i], dmul(tt, d[i]));
-  const float3 nrm = multi_normal<true>(M.s[0], M, s, off, isz, hp, d, err);
-  const float shade = fabsf(nrm.x * (float)d[0] + nrm.y * (float)d[1] + nrm.z * (float)d[2]);
-  const float4 base = classify(reinterpret_cast<const float4*>(s.lut), s.range_lo, 1.0f / (s.range_hi - s.range_lo),
-                               s.iso_threshold);
-  return make_float4(base.x * shade, base.y * shade, base.z * shade, 1.0f);
-}
-
-template <int DIM>
-__global__ void __launch_bounds__(kThreads, ISC_PROBE_MINB)
-    iso_probe_paired_kernel(const __grid_constant__ isc_render_args a, const __grid_constant__ MultiField M,
-                            int tiles_x, int tiles_y, int super_x, int n_codes, int* __restrict__ kend_px,
-                            float4* __restrict__ tail_px, int incl) {
-  const int lane = threadIdx.x & 31;
-  const int q = lane & 15, parity = lane >> 4;
-  const double* o = a.camera.origin;
-  const double step = a.step;
-  uint32_t* err = a.error_word;
-  const isc_source& s = a.src[0];
-  const MultiSrc& S = M.s[0];
-  const float thr = s.iso_threshold;
-  unsigned long long warp_stations = 0;
-
-  for (;;) {
-    int t = 0;
-    if (lane == 0) t = (int)atomicAdd(a.work_counter, 1u);
-    t = __shfl_sync(0xffffffffu, t, 0);
-    if (t >= n_codes) break;
-    const int sblk = t >> 6, w = t & 63;
-    const int tx = (sblk % super_x) * 8 + morton3(w, 0);
-    const int ty = (sblk / super_x) * 8 + morton3(w, 1);
-    if (tx >= tiles_x || ty >= tiles_y) continue;
-    const int px = tx * 8 + (q & 7), py = ty * 2 + (q >> 3);
-    const bool in_img = px < a.camera.width && py < a.camera.height;
-    Ray r;
-    if (in_img) {
-      setup_ray(a, px, py, r);
-    } else {
-      r.hit = false;
-      r.k_lo = r.k_hi = r.kg_lo = r.kg_hi = 0;
-    }
-    // guard interval (see march_multi_fast_kernel)
-    long long kend = r.k_hi;
-    bool bad_tail = false;
-    if (r.hit && r.k_hi > r.k_lo) {
-      double pa[3], pb[3];
-      station_pos(o, r.d, dmul((double)r.k_lo, step), pa);
-      station_pos(o, r.d, dmul((double)(r.k_hi - 1), step), pb);
-      if (!cell_guard_ok(M, pa)) {
-        if (err && !parity) atomicAdd(err, 1u);
-        kend = r.k_lo;
-      } else if (!cell_guard_ok(M, pb)) {
-        long long good = r.k_lo, bad = r.k_hi - 1;
-        while (bad - good > 1) {
-          const long long mid = good + ((bad - good) >> 1);
-          double pm[3];
-          station_pos(o, r.d, dmul((double)mid, step), pm);
-          if (cell_guard_ok(M, pm)) good = mid;
-          else bad = mid;
-        }
-        kend = bad;
-        bad_tail = true;
-      }
-    }
-    const long long n = (r.hit && kend > r.k_lo) ? (kend - r.k_lo) : 0;
-    const unsigned trips = __reduce_max_sync(0xffffffffu, (unsigned)((n + 1) >> 1));
-    double kd = (double)(r.k_lo + parity);
-    int left = (int)n - parity;
-    float prev = CUDART_NAN_F;           // even lane: value of the previous (odd) station
-    bool done = false;
-    long long my_k = -1;                 // this lane's hit station, if it decided the pair
-    double my_tau = 0.0, my_back = 0.0;  // its crossing (shaded after the loop, all lanes at once)
-    for (unsigned j = 0; j < trips; ++j, left -= 2, kd = dadd(kd, 2.0)) {
-      const bool valid = !done && left > 0;
-      float cur = CUDART_NAN_F;
-      double p[3];
-      if (valid) {
-        station_pos(o, r.d, dmul(kd, step), p);
-        int ix, iy, iz;
-        float fx, fy, fz;
-        cell_of(p, ix, iy, iz, fx, fy, fz);
-        float v[4] = {0.f, 0.f, 0.f, 0.f};
-        gather_guarded<DIM>(S, ix - M.lo[0], iy - M.lo[1], iz - M.lo[2], fx, fy, fz, v);
-        cur = run_chain_fast<DIM>(s, v);
-      }
-      const float from_even = __shfl_up_sync(0xffffffffu, cur, 16);
-      const float from_odd = __shfl_down_sync(0xffffffffu, cur, 16);
-      bool hit = false;
-      if (valid) {
-        const long long k = (long long)kd;
-        float before = parity ? from_even : prev;
-        if (k == r.k_lo && k - 1 >= r.kg_lo) before = iso_entry_value(a, M, r.d[0], r.d[1], r.d[2], k, err);
-        const float sa = before - thr, sb = cur - thr;
-        hit = isfinite(sa) && ((sa < 0.f) != (sb < 0.f));
-        double tau = 0.0, back = 0.0;
-        if (hit) {
-          const float den = sa - sb;
-          tau = den != 0.f ? (double)(sa / den) : 1.0;
-          back = -1.0;
-        } else if (k == r.k_hi - 1 && k + 1 < r.kg_hi) {  // exit pair, checked forward
-          double tau_x = 0.0;
-          hit = iso_exit_pair(a, M, r.d[0], r.d[1], r.d[2], k, p[0], p[1], p[2], sb, &tau_x, err);
-          tau = tau_x;
-        }
-        if (hit) {
-          my_k = k;
-          my_tau = tau;
-          my_back = back;
-        }
-      }
-      if (!parity) prev = from_odd;
-      // pair outcome: the even station is first; both lanes stop together
-      const bool hit_e = __shfl_sync(0xffffffffu, hit, q) != 0;
-      const bool hit_o = __shfl_sync(0xffffffffu, hit, q + 16) != 0;
-      if (parity && hit_e) my_k = -1;  // the even station decided the pair
-      done = done || hit_e || hit_o || left <= 2;
-      if (__all_sync(0xffffffffu, done)) break;  // every ray of the warp hit or ran out
-    }
-    if (bad_tail && !done && err && !parity) atomicAdd(err, 1u);  // marched into the bad tail
-    // Shade the hits here rather than in the loop: hits fall in different
-    // iterations, so in-loop shading ran once per hitting lane with the rest
-    // of the warp idle (the 6 gradient taps dominated the probe).
-    float4 my_c = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (my_k >= 0) {
-      double ph[3];
-      station_pos(o, r.d, dmul((double)my_k, step), ph);
-      my_c = iso_hit_color(a, M, r.d[0], r.d[1], r.d[2], ph[0], ph[1], ph[2], my_tau, my_back, err);
-    }
-    // resolve the pair's hit on the even lane
-    const long long ok = __shfl_down_sync(0xffffffffu, my_k, 16);
-    const float4 oc = make_float4(__shfl_down_sync(0xffffffffu, my_c.x, 16), __shfl_down_sync(0xffffffffu, my_c.y, 16),
-                                  __shfl_down_sync(0xffffffffu, my_c.z, 16), __shfl_down_sync(0xffffffffu, my_c.w, 16));
-    if (parity || !in_img) continue;
-    const long long hk = my_k >= 0 ? my_k : ok;
-    const float4 hc = my_k >= 0 ? my_c : oc;
-    const bool stopped = hk >= 0;
-    const uint32_t stations = stopped ? (uint32_t)(hk - r.k_lo + 1) : (uint32_t)n;
-    const long long pix = (long long)py * a.camera.width + px;
-    kend_px[pix] = (int)(stopped ? hk + incl : kend);
-    tail_px[pix] = stopped ? hc : make_float4(0.f, 0.f, 0.f, 0.f);
-    warp_stations += stations;
-    if (a.out_stations) a.out_stations[pix] = stations;
-    if (a.out_hit) a.out_hit[pix] = r.hit ? 1 : 0;
-    if (a.out_t) {
-      a.out_t[2 * pix] = r.t_in;
-      a.out_t[2 * pix + 1] = r.t_out;
-    }
-    if (a.out_krange)
-      reinterpret_cast<int4*>(a.out_krange)[pix] = make_int4((int)r.k_lo, (int)r.k_hi, (int)r.kg_lo, (int)r.kg_hi);
-  }
-  if (a.out_station_total) {
-#pragma unroll
-    for (int off2 = 16; off2 > 0; off2 >>= 1) warp_stations += __shfl_xor_sync(0xffffffffu, warp_stations, off2);
-    if (lane == 0 && warp_stations) atomicAdd(a.out_station_total, warp_stations);
-  }
-}
-
-template <int DIM>
-static int launch_iso_probe_paired(const isc_render_args* a, const MultiField& M, cudaStream_t st, int* kend_px,
-                                   float4* tail_px, int incl) {
-  const int tiles_x = (a->camera.width + 7) / 8, tiles_y = (a->camera.height + 1) / 2;
-  const int super_x = (tiles_x + 7) / 8, super_y = (tiles_y + 7) / 8;
-  const int n_codes = super_x * super_y * 64;
-  int dev = 0, sms = 148, per_sm = 1;
-  ISC_CUDA_CHECK(cudaGetDevice(&dev));
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, iso_probe_paired_kernel<DIM>, kThreads, 0);
-  int grid = sms * (per_sm > 0 ? per_sm : 1);
-  const int need = (n_codes + (kThreads / 32) - 1) / (kThreads / 32);
-  if (grid > need) grid = need > 0 ? need : 1;
-  iso_probe_paired_kernel<DIM><<<grid, kThreads, 0, st>>>(*a, M, tiles_x, tiles_y, super_x, n_codes, kend_px,
-                                                          tail_px, incl);
-  ISC_CUDA_CHECK(cudaGetLastError());
-  return ISC_OK;
-}
-
 static bool build_multi_field(const isc_render_args* a, MultiField& M);
-
-// Pass 1 of the iso + volume split (march.cu): `a` holds the iso source
-// alone; guarded trilinear float32 of 1 or 3 components.
-bool launch_iso_probe(const isc_render_args* a, cudaStream_t st, int* kend_px, float4* tail_px, int incl,
-                      int* status) {
-  MultiField M;
-  if (a->n_sources != 1 || !a->work_counter || !a->interpolation || !build_multi_field(a, M) || !M.s[0].guarded)
-    return false;
-  switch (a->src[0].feature_dim) {
-    case 1: *status = launch_iso_probe_paired<1>(a, M, st, kend_px, tail_px, incl); return true;
-    case 3: *status = launch_iso_probe_paired<3>(a, M, st, kend_px, tail_px, incl); return true;
-    default: return false;
-  }
-}
 
 // Returns true (and the launch status in *status) when the multi kernel
 // handles this render: 1..4 float32 sources, 32-bit offsets, work counter.
