@@ -395,6 +395,17 @@ __global__ void __launch_bounds__(kThreads, ISC_MULTI_FAST_MINB)
 
     Ray r;
     setup_ray(a, px, py, r);
+    const long long pix = (long long)py * a.camera.width + px;
+    // parity / debug outputs first: the slab intervals are then dead during the march
+    if (a.out_hit) a.out_hit[pix] = r.hit ? 1 : 0;
+    if (a.out_t) {
+      a.out_t[2 * pix] = r.t_in;
+      a.out_t[2 * pix + 1] = r.t_out;
+    }
+    if (a.out_krange)
+      reinterpret_cast<int4*>(a.out_krange)[pix] = make_int4((int)r.k_lo, (int)r.k_hi, (int)r.kg_lo, (int)r.kg_hi);
+    // station indices as int for the march (a ray holds < 2^31 stations)
+    const int k_lo = (int)r.k_lo, k_hi = (int)r.k_hi, kg_lo = (int)r.kg_lo, kg_hi = (int)r.kg_hi;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     uint32_t stations = 0;
     // Stations whose gathers honour the guard form one interval (each cell
@@ -426,8 +437,9 @@ __global__ void __launch_bounds__(kThreads, ISC_MULTI_FAST_MINB)
     }
     bool stopped = false;
     int hit_si = -1;                     // first iso source hit (shaded after the loop)
-    long long hit_k = 0;
-    double hit_tau = 0.0, hit_back = 0.0;
+    int hit_k = 0;
+    double hit_tau = 0.0;
+    bool hit_behind = false;             // crossing between k-1 and k (back = -1) rather than k and k+1
     float4 hit_front = make_float4(0.f, 0.f, 0.f, 0.f);  // the station's sources in front of it
     if (r.hit) {
       float prev[NS];
@@ -469,8 +481,8 @@ __global__ void __launch_bounds__(kThreads, ISC_MULTI_FAST_MINB)
           // ---- iso: raycast.py:384-468 (every source here is guarded: "exact") ----
           const float thr = s.iso_threshold;
           float before = prev[si];
-          const long long k = (long long)kd;
-          if (k == r.k_lo && k - 1 >= r.kg_lo) {  // entry pair: sample k-1 through the guard
+          const int k = (int)kd;
+          if (k == k_lo && k - 1 >= kg_lo) {  // entry pair: sample k-1 through the guard
             double off[3], bsz[3], pq[3];
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
@@ -488,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, ISC_MULTI_FAST_MINB)
             tau = den != 0.f ? (double)(sa / den) : 1.0;
             back = -1.0;
           }
-          if (!hit && k == r.k_hi - 1 && k + 1 < r.kg_hi) {  // exit pair, checked forward
+          if (!hit && k == k_hi - 1 && k + 1 < kg_hi) {  // exit pair, checked forward
             double off[3], bsz[3], vb[3], pn[3], noff[3];
             station_pos(o, r.d, dmul((double)(k + 1), step), pn);
 #pragma unroll
@@ -515,7 +527,7 @@ __global__ void __launch_bounds__(kThreads, ISC_MULTI_FAST_MINB)
             hit_si = si;
             hit_k = k;
             hit_tau = tau;
-            hit_back = back;
+            hit_behind = back != 0.0;
             hit_front = st;
             stop = true;
           }
@@ -537,21 +549,13 @@ __global__ void __launch_bounds__(kThreads, ISC_MULTI_FAST_MINB)
     if (hit_si >= 0) {
       double ph[3];
       station_pos(o, r.d, dmul((double)hit_k, step), ph);
-      const float4 c = iso_hit_color(a, M, hit_si, r.d[0], r.d[1], r.d[2], ph[0], ph[1], ph[2], hit_tau, hit_back,
-                                     err);
+      const float4 c = iso_hit_color(a, M, hit_si, r.d[0], r.d[1], r.d[2], ph[0], ph[1], ph[2], hit_tau,
+                                     hit_behind ? -1.0 : 0.0, err);
       acc = over4(acc, over4(hit_front, c));
     }
-    const long long pix = (long long)py * a.camera.width + px;
     reinterpret_cast<float4*>(a.out_rgba)[pix] = acc;
     warp_stations += stations;
     if (a.out_stations) a.out_stations[pix] = stations;
-    if (a.out_hit) a.out_hit[pix] = r.hit ? 1 : 0;
-    if (a.out_t) {
-      a.out_t[2 * pix] = r.t_in;
-      a.out_t[2 * pix + 1] = r.t_out;
-    }
-    if (a.out_krange)
-      reinterpret_cast<int4*>(a.out_krange)[pix] = make_int4((int)r.k_lo, (int)r.k_hi, (int)r.kg_lo, (int)r.kg_hi);
   }
   if (a.out_station_total) {
 #pragma unroll
