@@ -15,11 +15,17 @@ from . import _abi
 _DTYPES = {torch.float32: _abi.F32, torch.float64: _abi.F64, torch.float16: _abi.F16, torch.bfloat16: _abi.BF16}
 
 
+_CUDA_OK = False
+
+
 def require_cuda() -> torch.device:
-    if not torch.cuda.is_available():
-        raise RuntimeError("paper_1611_09048_b200 renders on a CUDA device (sm_100a); none is available "
-                           "and there is no CPU fallback")
-    _abi.lib()
+    global _CUDA_OK
+    if not _CUDA_OK:
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_1611_09048_b200 renders on a CUDA device (sm_100a); none is available "
+                               "and there is no CPU fallback")
+        _abi.lib()
+        _CUDA_OK = True
     return torch.device("cuda", torch.cuda.current_device())
 
 

@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import threading
 from dataclasses import dataclass
 from typing import Callable, Optional, Sequence
 
@@ -204,10 +205,28 @@ def pack_render_args(domain, volume, scene: SceneState, plans: Sequence[SourcePl
     return a
 
 
+_LINE_CACHE: dict = {}
+_LINE_LOCK = threading.Lock()
+
+
 def lut_line(lut: np.ndarray, tol: float = 1e-12):
     """(base, slope) if all 256 LUT entries lie on one line in x = 0..255
-    (so the LUT lerp equals base + slope * x), else None."""
+    (so the LUT lerp equals base + slope * x), else None.  Memoised on the LUT
+    bytes (a transfer function changes only when steered)."""
     lut = np.asarray(lut, dtype=np.float64)
+    key = (lut.tobytes(), tol)
+    with _LINE_LOCK:
+        if key in _LINE_CACHE:
+            return _LINE_CACHE[key]
+    res = _lut_line(lut, tol)
+    with _LINE_LOCK:
+        if len(_LINE_CACHE) > 256:
+            _LINE_CACHE.clear()
+        _LINE_CACHE[key] = res
+    return res
+
+
+def _lut_line(lut: np.ndarray, tol: float):
     second = lut[2:] - 2.0 * lut[1:-1] + lut[:-2]
     if np.abs(second).max() > tol:
         return None
