@@ -161,6 +161,16 @@ typedef struct {
                                 (LocalImage.stations, raycast.py:46); optional */
   uint32_t* work_counter;    /* device u32 scratch for the persistent tile
                                 scheduler; optional (null = static grid) */
+  /* Ray-list mode (raycast.march_rays, raycast.py:291-381, and march_ray,
+   * 471-489): when ray_dirs is set, the "image" is camera.width x
+   * camera.height rays whose directions (float64 x3, used as given, not
+   * normalised) and intervals (float64 x4: brick t0, t1, global t0, t1) are
+   * read from these device arrays instead of being derived from the camera;
+   * camera.origin is the common origin, clip planes are not applied (the
+   * intervals are final) and every ray marches k in
+   * [ceil(max(t0,0)/step), ceil(max(t1,0)/step)).  Null in a frame render. */
+  const double* ray_dirs;
+  const double* ray_intervals;
 } isc_render_args;
 /* isc_render_local zeroes *error_word, *out_station_total and *work_counter
  * (stream-ordered) before the march, so callers never need a separate fill. */
@@ -179,6 +189,12 @@ ISC_API int isc_device_sm_count(int device);
 ISC_API int isc_render_local(const isc_render_args* args, void* stream);
 /* Ray setup only (parity/debug): fills out_t / out_krange / out_hit. */
 ISC_API int isc_ray_setup(const isc_render_args* args, void* stream);
+/* Central-difference normals of src[0]'s chained scalar at n positions
+ * (raycast.gradient_normals, raycast.py:210-242): stencil clamped to the
+ * samplable box of the brick, zero gradient -> -view_dir.  positions and
+ * view_dirs are device float64 (n, 3); out_normals device float32 (n, 3). */
+ISC_API int isc_gradient_normals(const isc_render_args* args, const double* positions, const double* view_dirs,
+                                 int64_t n, float* out_normals, void* stream);
 /* Per-source normalisation: (min, max) of the float32-chained first
  * component over the brick interior (guard excluded), NaN ignored.
  * out_minmax: device buffer of >= 4 32-bit words; [0], [1] receive (min, max)

@@ -22,13 +22,18 @@ from .transport import (LocalFabric, LocalNvlinkGroup, LocalTransport, NvlinkTra
 
 def __getattr__(name):
     # Device-side modules import torch lazily so host-only use stays light.
-    if name in ("LocalImage", "SourcePlan", "build_plans", "render_local", "RankContext", "ray_box_intersection"):
+    if name in ("LocalImage", "SourcePlan", "build_plans", "render_local", "RankContext", "ray_box_intersection",
+                "march_rays", "march_ray", "gradient_normals", "gradient_normal"):
         from . import raycast
         return getattr(raycast, name)
     if name in ("binary_swap", "composite_sequential", "over", "over_arrays", "visibility_order",
                 "CompositeMessage"):
         from . import compositing
         return getattr(compositing, name)
+    if name in ("FrameStreamer", "broadcast_scene", "encode_frame", "decode_frame", "frame_pipeline",
+                "merge_metadata", "to_rgba8", "PipelineContext"):
+        from . import runtime
+        return getattr(runtime, name)
     if name in ("value_range", "auto_value_ranges"):
         from . import normalize
         return getattr(normalize, name)

@@ -96,6 +96,8 @@ class RenderArgs(C.Structure):
         ("error_word", C.c_void_p),
         ("out_station_total", C.c_void_p),
         ("work_counter", C.c_void_p),
+        ("ray_dirs", C.c_void_p),
+        ("ray_intervals", C.c_void_p),
     ]
 
 
@@ -145,6 +147,8 @@ _SIGNATURES = {
     "isc_device_sm_count": (C.c_int, [C.c_int]),
     "isc_render_local": (C.c_int, [C.POINTER(RenderArgs), C.c_void_p]),
     "isc_ray_setup": (C.c_int, [C.POINTER(RenderArgs), C.c_void_p]),
+    "isc_gradient_normals": (C.c_int, [C.POINTER(RenderArgs), C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                       C.c_void_p]),
     "isc_value_range": (C.c_int, [C.POINTER(Source), C.POINTER(C.c_int32), C.c_int32, C.c_void_p, C.c_void_p]),
     "isc_over": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "isc_composite_fold": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.c_int32, C.c_int64, C.c_void_p]),

@@ -406,6 +406,20 @@ __global__ void __launch_bounds__(kThreads, ISC_FAST_MINB) march_fast_kernel(con
   }
 }
 
+// raycast.gradient_normals (raycast.py:210-242) at caller positions.
+__global__ void gradient_kernel(const __grid_constant__ isc_render_args a, const double* __restrict__ pos,
+                                const double* __restrict__ view, long long n, float* __restrict__ out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const Brick b = make_brick(a);
+  const double p[3] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+  const double d[3] = {view[3 * i], view[3 * i + 1], view[3 * i + 2]};
+  const float3 nn = iso_normal(a.src[0], b, p, d, a.interpolation != 0, a.error_word);
+  out[3 * i] = nn.x;
+  out[3 * i + 1] = nn.y;
+  out[3 * i + 2] = nn.z;
+}
+
 __global__ void __launch_bounds__(kThreads) ray_setup_kernel(const __grid_constant__ isc_render_args a) {
   int px, py;
   tile_pixel(px, py);
@@ -541,6 +555,22 @@ extern "C" int isc_render_local(const isc_render_args* a, void* stream) {
   const size_t smem = (size_t)a->n_sources * ISC_LUT_ENTRIES * sizeof(float4);
   if (a->interpolation) march_kernel<true><<<grid, kThreads, smem, s>>>(*a);
   else march_kernel<false><<<grid, kThreads, smem, s>>>(*a);
+  ISC_CUDA_CHECK(cudaGetLastError());
+  return ISC_OK;
+}
+
+extern "C" int isc_gradient_normals(const isc_render_args* a, const double* positions, const double* view_dirs,
+                                    int64_t n, float* out_normals, void* stream) {
+  int st = validate(a, false);
+  if (st != ISC_OK) return st;
+  if (a->n_sources < 1) return fail(ISC_E_VALUE, "gradient_normals needs a source in src[0]");
+  if (n < 0) return fail(ISC_E_VALUE, "negative position count");
+  if (n == 0) return ISC_OK;
+  if (!positions || !view_dirs || !out_normals) return fail(ISC_E_VALUE, "null positions / view_dirs / output");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (a->error_word) ISC_CUDA_CHECK(cudaMemsetAsync(a->error_word, 0, sizeof(uint32_t), s));
+  const int threads = 128;
+  gradient_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, s>>>(*a, positions, view_dirs, n, out_normals);
   ISC_CUDA_CHECK(cudaGetLastError());
   return ISC_OK;
 }

@@ -78,6 +78,22 @@ __device__ __forceinline__ long long station_ceil(double t, double step) {
 }
 
 __device__ __forceinline__ void setup_ray(const isc_render_args& a, int px, int py, Ray& r) {
+  if (a.ray_dirs) {  // ray-list mode (march_rays): direction and intervals given
+    const long long i = (long long)py * a.camera.width + px;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) r.d[k] = a.ray_dirs[3 * i + k];
+    r.t_in = a.ray_intervals[4 * i];
+    r.t_out = a.ray_intervals[4 * i + 1];
+    r.g_in = a.ray_intervals[4 * i + 2];
+    r.g_out = a.ray_intervals[4 * i + 3];
+    r.hit = true;
+    r.k_lo = station_ceil(r.t_in, a.step);
+    r.k_hi = station_ceil(r.t_out, a.step);
+    r.kg_lo = station_ceil(r.g_in, a.step);
+    r.kg_hi = station_ceil(r.g_out, a.step);
+    if (r.k_hi < r.k_lo) r.k_hi = r.k_lo;
+    return;
+  }
   const isc_camera& c = a.camera;
   ray_direction(c, px, py, r.d);
   double lo[3], hi[3], glo[3], ghi[3];

@@ -31,7 +31,7 @@ from .device import LUTS, as_device_field, dtype_code, ptr, require_cuda, stream
 from .errors import FieldError, GuardContractError
 from .fields import LocalDomain, SourceHandle, SourceRegistry
 from .functors import ChainLimits, FunctorChain, FunctorRegistry, device_program, parse_chain
-from .scene import ISO_MODE, SceneState, TransferFunction
+from .scene import ISO_MODE, Camera, RenderSettings, SceneState, TransferFunction
 
 StationRecorder = Callable[[int, np.ndarray], None]
 
@@ -328,6 +328,110 @@ def _replay_stations(recorder: StationRecorder, counts: torch.Tensor, kr: torch.
         sel = live[(start <= k) & (k < stop)]
         if sel.size:
             recorder(k, sel)
+
+
+class _RayListScene:
+    """What pack_render_args reads from a scene, for ray-list launches: the
+    camera supplies only the common origin (directions come from the list)."""
+
+    def __init__(self, origin, n, settings):
+        o = tuple(float(v) for v in origin)
+        self.camera = Camera(o, (o[0], o[1], o[2] + 1.0), image_size=(max(int(n), 1), 1))
+        self.settings = settings
+        self.clip_planes = ()
+
+
+class _WholeVolume:
+    """march_rays(volume=None): the brick is the whole volume (no neighbour
+    owns an iso pair; entry pairs come from the global interval only)."""
+
+    def __init__(self, domain):
+        self.size = tuple(int(domain.offset[a]) + int(domain.size[a]) for a in range(3))
+        self.decomposition = (1, 1, 1)
+
+
+def march_rays(origin, dirs, local_interval, global_interval, plans: Sequence[SourcePlan], settings,
+               station_recorder: Optional[StationRecorder] = None, volume=None):
+    """March explicit rays on the device (raycast.py:291-381): every ray i
+    marches the stations k in [ceil(max(t0_i,0)/step), ceil(max(t1_i,0)/step))
+    from ``origin`` along ``dirs[i]`` (used as given).  Returns
+    ((n, 4) float64 premultiplied RGBA, stations marched).  The same kernels
+    as ``render_local`` run, in ray-list mode (isc_render_args.ray_dirs)."""
+    device = require_cuda()
+    d = np.asarray(dirs, dtype=np.float64).reshape(-1, 3)
+    n = d.shape[0]
+    if n == 0 or not plans:
+        return np.zeros((n, 4)), 0
+    t0 = np.asarray(local_interval[0], dtype=np.float64).reshape(-1)
+    t1 = np.asarray(local_interval[1], dtype=np.float64).reshape(-1)
+    g0 = np.asarray(global_interval[0], dtype=np.float64).reshape(-1)
+    g1 = np.asarray(global_interval[1], dtype=np.float64).reshape(-1)
+    domain = plans[0].domain
+    vol = volume if volume is not None else _WholeVolume(domain)
+    keep: list = []
+    args = pack_render_args(domain, vol, _RayListScene(origin, n, settings), plans, device, keep)
+    dirs_t = torch.from_numpy(np.ascontiguousarray(d)).to(device)
+    iv_t = torch.from_numpy(np.ascontiguousarray(np.stack([t0, t1, g0, g1], axis=1))).to(device)
+    out = torch.empty((1, n, 4), dtype=torch.float32, device=device)
+    counts = torch.empty(n, dtype=torch.int32, device=device) if station_recorder is not None else None
+    kr = torch.empty((n, 4), dtype=torch.int32, device=device) if station_recorder is not None else None
+    stats = torch.zeros(3, dtype=torch.int64, device=device)
+    args.ray_dirs, args.ray_intervals = ptr(dirs_t), ptr(iv_t)
+    args.out_rgba = ptr(out)
+    args.out_stations = ptr(counts) if counts is not None else None
+    args.out_krange = ptr(kr) if kr is not None else None
+    args.out_station_total = ptr(stats)
+    args.error_word = ptr(stats) + 8
+    args.work_counter = ptr(stats) + 16
+    _abi.check(_abi.lib().isc_render_local(C.byref(args), C.c_void_p(stream_handle(None))), "march_rays")
+    torch.cuda.current_stream().synchronize()
+    if int(stats[1].item()):
+        raise GuardContractError(f"{int(stats[1].item())} trilinear reads beyond the guard halo")
+    if station_recorder is not None:
+        _replay_stations(station_recorder, counts, kr)
+    stations = int(stats[0].item())
+    taps = 8 if settings.interpolation else 1
+    for plan in plans:
+        plan.handle.add_device_samples(lambda st=stations, taps=taps: taps * st)
+    return out.reshape(n, 4).double().cpu().numpy(), stations
+
+
+def march_ray(origin, direction, interval, plans: Sequence[SourcePlan], settings, global_interval=None):
+    """Single-ray convenience wrapper over :func:`march_rays` (raycast.py:471-489)."""
+    gi = global_interval if global_interval is not None else interval
+    rgba, _ = march_rays(origin, [direction], ([interval[0]], [interval[1]]), ([gi[0]], [gi[1]]), plans, settings)
+    return rgba[0]
+
+
+def gradient_normals(plan: SourcePlan, pos, view_dirs, interpolation: bool) -> np.ndarray:
+    """Central-difference normals of the plan's chained scalar on the device
+    (raycast.py:210-242, isc_gradient_normals); (n, 3) float64."""
+    device = require_cuda()
+    p = np.ascontiguousarray(np.asarray(pos, dtype=np.float64).reshape(-1, 3))
+    v = np.ascontiguousarray(np.asarray(view_dirs, dtype=np.float64).reshape(-1, 3))
+    n = p.shape[0]
+    if n == 0:
+        return np.zeros((0, 3))
+    settings = RenderSettings(active_set=(plan.source_id,), interpolation=bool(interpolation))
+    keep: list = []
+    args = pack_render_args(plan.domain, _WholeVolume(plan.domain), _RayListScene((0.0, 0.0, 0.0), n, settings),
+                            [plan], device, keep)
+    p_t, v_t = torch.from_numpy(p).to(device), torch.from_numpy(v).to(device)
+    out = torch.empty((n, 3), dtype=torch.float32, device=device)
+    err = torch.zeros(1, dtype=torch.int32, device=device)
+    args.error_word = ptr(err)
+    _abi.check(_abi.lib().isc_gradient_normals(C.byref(args), C.c_void_p(ptr(p_t)), C.c_void_p(ptr(v_t)), n,
+                                               C.c_void_p(ptr(out)), C.c_void_p(stream_handle(None))),
+               "gradient_normals")
+    torch.cuda.current_stream().synchronize()
+    if int(err.item()):
+        raise GuardContractError(f"{int(err.item())} trilinear reads beyond the guard halo")
+    return out.double().cpu().numpy()
+
+
+def gradient_normal(plan: SourcePlan, position, view_dir, interpolation: bool = True) -> np.ndarray:
+    """Single-point wrapper over :func:`gradient_normals` (raycast.py:245-256)."""
+    return gradient_normals(plan, [position], [view_dir], interpolation)[0]
 
 
 def ray_box_intersection(origin, direction, box_lo, box_hi, clip_planes=()):
