@@ -246,7 +246,7 @@ template <bool INTERP, bool GUARDED, bool PAIRED, bool LINE = false, int DIM = 1
 __global__ void __launch_bounds__(kThreads, ISC_FAST_MINB) march_fast_kernel(const __grid_constant__ isc_render_args a,
                                                               const FastField F, int tiles_x, int tiles_y,
                                                               int super_x, int n_codes, int row_order,
-                                                              int tw_log2) {
+                                                              int tw_log2, int tile_x0, int tile_y0) {
   __shared__ float4 lut_s[ISC_LUT_ENTRIES];
   for (int i = threadIdx.x; i < ISC_LUT_ENTRIES; i += blockDim.x)
     lut_s[i] = reinterpret_cast<const float4*>(a.src[0].lut)[i];
@@ -280,6 +280,8 @@ __global__ void __launch_bounds__(kThreads, ISC_FAST_MINB) march_fast_kernel(con
       ty = (sblk / super_x) * 8 + morton3(w, 1);
     }
     if (tx >= tiles_x || ty >= tiles_y) continue;
+    tx += tile_x0;  // tiles of the brick's screen rectangle only
+    ty += tile_y0;
     const int px = tx * tw + (q & (tw - 1)), py = ty * th + (q >> tw_log2);
     const bool in_img = px < a.camera.width && py < a.camera.height;
     if (!PAIRED && !in_img) continue;
@@ -508,7 +510,19 @@ template <bool INTERP, bool GUARDED, bool PAIRED, bool LINE = false, int DIM = 1
 static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_t st) {
   static const int tw_log2 = getenv("ISC_TILE_W") ? __builtin_ctz(atoi(getenv("ISC_TILE_W"))) : 3;
   const int tw = 1 << tw_log2, th = (PAIRED ? 16 : 32) >> tw_log2;
-  const int tiles_x = (a->camera.width + tw - 1) / tw, tiles_y = (a->camera.height + th - 1) / th;
+  int tiles_x = (a->camera.width + tw - 1) / tw, tiles_y = (a->camera.height + th - 1) / th;
+  int tile_x0 = 0, tile_y0 = 0;
+  int rx0, ry0, rx1, ry1;
+  static const bool no_cull = getenv("ISC_DISABLE_CULL") != nullptr;
+  if (!no_cull && brick_screen_rect(a, rx0, ry0, rx1, ry1)) {
+    // pixels outside the rectangle miss the brick: transparent
+    ISC_CUDA_CHECK(cudaMemsetAsync(a->out_rgba, 0, (size_t)a->camera.width * a->camera.height * sizeof(float4), st));
+    tile_x0 = rx0 / tw;
+    tile_y0 = ry0 / th;
+    tiles_x = rx1 > rx0 ? (rx1 + tw - 1) / tw - tile_x0 : 0;
+    tiles_y = ry1 > ry0 ? (ry1 + th - 1) / th - tile_y0 : 0;
+    if (tiles_x == 0 || tiles_y == 0) return ISC_OK;
+  }
   const int super_x = (tiles_x + 7) / 8, super_y = (tiles_y + 7) / 8;
   static const bool row_order = getenv("ISC_TILE_ROWS") != nullptr;
   const int n_codes = row_order ? tiles_x * tiles_y : super_x * super_y * 64;
@@ -521,7 +535,7 @@ static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_
   const int need = (total_warps + (kThreads / 32) - 1) / (kThreads / 32);
   if (grid > need) grid = need > 0 ? need : 1;
   march_fast_kernel<INTERP, GUARDED, PAIRED, LINE, DIM><<<grid, kThreads, 0, st>>>(
-      *a, F, tiles_x, tiles_y, super_x, n_codes, row_order ? 1 : 0, tw_log2);
+      *a, F, tiles_x, tiles_y, super_x, n_codes, row_order ? 1 : 0, tw_log2, tile_x0, tile_y0);
   ISC_CUDA_CHECK(cudaGetLastError());
   return ISC_OK;
 }

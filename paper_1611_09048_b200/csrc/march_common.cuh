@@ -117,6 +117,42 @@ __device__ __forceinline__ void fast_gather(const FastField& F, const double p[3
   }
 }
 
+// Host: conservative pixel rectangle [x0, x1) x [y0, y1) outside which no
+// primary ray can hit the brick -- the bounding box of the pinhole projection
+// of the brick's 8 corners (the image of a box in front of the camera is the
+// convex hull of its projected corners), widened by 2 px against rounding.
+// False (no culling) when a corner is not strictly in front of the camera,
+// for explicit ray lists, and when per-pixel debug outputs are requested
+// (they are defined for every pixel).
+inline bool brick_screen_rect(const isc_render_args* a, int& x0, int& y0, int& x1, int& y1) {
+  if (a->ray_dirs || a->out_stations || a->out_hit || a->out_t || a->out_krange) return false;
+  const isc_camera& c = a->camera;
+  double xmin = 1e300, xmax = -1e300, ymin = 1e300, ymax = -1e300;
+  for (int corner = 0; corner < 8; ++corner) {
+    double v[3];
+    for (int i = 0; i < 3; ++i)
+      v[i] = a->brick_offset[i] + ((corner >> i) & 1 ? a->brick_size[i] : 0) - c.origin[i];
+    const double depth = v[0] * c.fwd[0] + v[1] * c.fwd[1] + v[2] * c.fwd[2];
+    const double len = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+    if (!(depth > 1e-6 * len) || !(depth > 0.0)) return false;
+    const double col = (v[0] * c.right[0] + v[1] * c.right[1] + v[2] * c.right[2]) / (depth * c.tan_half * c.aspect);
+    const double row = (v[0] * c.up[0] + v[1] * c.up[1] + v[2] * c.up[2]) / (depth * c.tan_half);
+    const double px = (col + 1.0) * 0.5 * c.width - 0.5, py = (1.0 - row) * 0.5 * c.height - 0.5;
+    xmin = fmin(xmin, px);
+    xmax = fmax(xmax, px);
+    ymin = fmin(ymin, py);
+    ymax = fmax(ymax, py);
+  }
+  auto clampi = [](double v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : (int)v); };
+  x0 = clampi(floor(xmin) - 2.0, 0, c.width);
+  y0 = clampi(floor(ymin) - 2.0, 0, c.height);
+  x1 = clampi(ceil(xmax) + 3.0, 0, c.width);
+  y1 = clampi(ceil(ymax) + 3.0, 0, c.height);
+  if (x1 < x0) x1 = x0;
+  if (y1 < y0) y1 = y0;
+  return true;
+}
+
 __device__ __forceinline__ int morton3(int w, int shift) {
   return ((w >> shift) & 1) | (((w >> (shift + 2)) & 1) << 1) | (((w >> (shift + 4)) & 1) << 2);
 }

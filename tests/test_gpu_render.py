@@ -407,3 +407,45 @@ def test_analytic_single_ramp_classification_equals_lut_path():
     assert np.abs(fast - gold["d111_r0_rgba"]).max() <= RGBA_TOL
     warm = P.tf_from_points(cases.WARM_TF, (0.0, 1.0))
     assert lut_line(warm.lut) is None
+
+
+@pytest.mark.parametrize("multi", [False, True])
+def test_screen_rect_culling_is_exact(multi):
+    """Without per-pixel debug outputs the persistent kernels only schedule
+    tiles inside the brick's projected screen rectangle (and clear the rest);
+    the image must be bit-identical to the full-raster render (debug outputs
+    requested), for every brick of a 2x2x2 decomposition and cameras outside,
+    grazing and inside the volume."""
+    import paper_1611_09048_b200 as P
+    torch = _torch()
+    n = 32
+    rng = np.random.default_rng(17)
+    full = rng.random((n + 2, n + 2, n + 2)).astype(np.float32)
+    vec = rng.random((n + 2, n + 2, n + 2, 3)).astype(np.float32)
+    vol = P.GlobalVolume((n, n, n), (2, 2, 2))
+    cams = [((70.0, 50.0, -40.0), (16.0, 16.0, 16.0)), ((16.0, 90.0, 16.5), (16.0, 16.0, 16.0)),
+            ((-3.0, 5.0, 4.0), (30.0, 20.0, 28.0)), ((15.0, 17.0, 14.0), (0.0, 40.0, 30.0))]
+    for r in range(8):
+        dom = vol.local_domain(r, 1)
+        ox, oy, oz = dom.offset
+        reg = P.SourceRegistry(dom)
+        sl = np.s_[oz:oz + 18, oy:oy + 18, ox:ox + 18]
+        reg.register_handle(P.array_backed_handle(P.SourceDescriptor("s", 1, has_guard=True),
+                                                  torch.from_numpy(np.ascontiguousarray(full[sl])).cuda(), 1))
+        reg.register_handle(P.array_backed_handle(P.SourceDescriptor("v", 3, has_guard=True),
+                                                  torch.from_numpy(np.ascontiguousarray(vec[sl])).cuda(), 1))
+        active = (0, 1) if multi else (0,)
+        P.update_sources(reg, set(active), {})
+        fr = P.default_registry()
+        ctx = P.RankContext(vol, dom, reg, fr, fr.limits)
+        for pos, look in cams:
+            scene = P.SceneState(
+                camera=P.Camera(pos, look, image_size=(64, 48)),
+                tf_points={0: [(0.0, 0.0, 0.0, 0.0, 0.0), (1.0, 1.0, 0.5, 0.2, 0.6)],
+                           1: [(0.0, 0.0, 0.0, 0.0, 0.0), (1.0, 0.2, 0.9, 1.0, 0.4)]},
+                value_ranges={0: (0.0, 1.0), 1: (0.0, 2.0)}, chain_texts={0: "", 1: "length"},
+                settings=P.RenderSettings(active_set=active, modes={0: "iso"} if multi else {},
+                                          iso_thresholds={0: 0.5}, early_termination_alpha=1.0))
+            culled = P.render_local(ctx, scene).pixels.cpu().numpy()
+            fullraster = P.render_local(ctx, scene, keep_station_counts=True).pixels.cpu().numpy()
+            assert np.array_equal(culled, fullraster), (r, pos)
