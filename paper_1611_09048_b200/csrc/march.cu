@@ -227,7 +227,8 @@ __global__ void __launch_bounds__(kThreads) march_kernel(const __grid_constant__
 // cache lines per request than an 8x4 tile).  Each station pair is merged in
 // order with one shuffle exchange: pair = s_even over s_odd, acc = acc over
 // pair -- the same over-sequence as the reference's per-station loop.
-// Used when early termination is off (alpha_stop >= 1).
+// ET (early termination, alpha_stop < 1): the even lane composites station by
+// station with the stop test after each.
 // Straight RGBA of a transfer function whose LUT is one straight run
 // (isc_source.lut_linear): identical to the LUT lerp, no shared-memory lookup.
 // Returns the PREMULTIPLIED colour; a non-finite value gets alpha 0 (and so
@@ -242,7 +243,7 @@ __device__ __forceinline__ float4 classify_line_premul(const isc_source& s, floa
 #ifndef ISC_FAST_MINB
 #define ISC_FAST_MINB 4  // <= 64 registers: 4 CTAs (32 warps) per SM
 #endif
-template <bool INTERP, bool GUARDED, bool PAIRED, bool LINE = false, int DIM = 1>
+template <bool INTERP, bool GUARDED, bool PAIRED, bool LINE = false, int DIM = 1, bool ET = false>
 __global__ void __launch_bounds__(kThreads, ISC_FAST_MINB) march_fast_kernel(const __grid_constant__ isc_render_args a,
                                                               const FastField F, int tiles_x, int tiles_y,
                                                               int super_x, int n_codes, int row_order,
@@ -303,26 +304,42 @@ __global__ void __launch_bounds__(kThreads, ISC_FAST_MINB) march_fast_kernel(con
       const long long k_hi = r.k_hi;
       const long long n = r.hit ? (k_hi - r.k_lo) : 0;
       long long nm = n;  // stations this lane pair marches
-#ifndef ISC_EXP_SAMPLE_GUARD
+      bool bad_tail = false;
       // Guard contract checked once per ray: every axis of the station
       // position o + (k*step)*d is a composition of monotone roundings, so
-      // each cell index is monotone in k and the base cells of the first and
-      // last station bound those of every station between them.  A violating
-      // ray is not marched (the call reports GuardContractError, as the
-      // reference raises on the first bad gather, fields.py:230-238).
+      // each cell index is monotone in k and the stations whose gathers
+      // honour the halo form one interval.  Without early termination every
+      // station is gathered: a bad first or last station is the reference's
+      // GuardContractError (fields.py:230-238) and the ray is not marched.
+      // With early termination the ray may stop before a bad tail: march up
+      // to the last good station (binary search) and report the error only
+      // if the ray gets there.
       if (GUARDED && n > 0) {
         double pa[3], pb[3];
         station_pos(o, r.d, dmul((double)r.k_lo, step), pa);
         station_pos(o, r.d, dmul((double)(k_hi - 1), step), pb);
-        if (!guard_ok(F, pa) || !guard_ok(F, pb)) {
+        if (!guard_ok(F, pa)) {
           if (err && !parity) atomicAdd(err, 1u);
           nm = 0;
+        } else if (!guard_ok(F, pb)) {
+          if constexpr (ET) {
+            long long good = r.k_lo, bad = k_hi - 1;
+            while (bad - good > 1) {
+              const long long mid = good + ((bad - good) >> 1);
+              double pm[3];
+              station_pos(o, r.d, dmul((double)mid, step), pm);
+              if (guard_ok(F, pm)) good = mid;
+              else bad = mid;
+            }
+            nm = bad - r.k_lo;
+            bad_tail = true;
+          } else {
+            if (err && !parity) atomicAdd(err, 1u);
+            nm = 0;
+          }
         }
       }
       constexpr bool kCheck = false;
-#else
-      constexpr bool kCheck = true;
-#endif
       const unsigned pairs = (unsigned)((nm + 1) >> 1);
       const unsigned trips = __reduce_max_sync(0xffffffffu, pairs);
       // station index as an exact float64 integer (k < 2^53) stepped by 2.0:
@@ -330,9 +347,11 @@ __global__ void __launch_bounds__(kThreads, ISC_FAST_MINB) march_fast_kernel(con
       // remaining stations.
       double kd = (double)(r.k_lo + parity);
       int left = (int)nm - parity;
+      bool done = false;        // ET: the pair's ray reached alpha_stop
+      uint32_t marched = 0;     // ET: stations composited (even lane)
       for (unsigned j = 0; j < trips; ++j, left -= 2, kd = dadd(kd, 2.0)) {
         float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (left > 0) {
+        if (left > 0 && !(ET && done)) {
           double p0[3];
           station_pos(o, r.d, dmul(kd, step), p0);
           float s0;
@@ -352,9 +371,33 @@ __global__ void __launch_bounds__(kThreads, ISC_FAST_MINB) march_fast_kernel(con
         // it takes the odd lane's sample with a shuffle-down and composites
         // even-over-odd; the odd lane's accumulator is dead.
         const float4 odd = shfl_down16(c);
-        acc = over4(acc, over4(c, odd));
+        if constexpr (!ET) {
+          acc = over4(acc, over4(c, odd));
+        } else {
+          // early termination (raycast.py:377-380): station by station, the
+          // stop test after each one, exactly as the reference's loop
+          if (!parity && !done) {
+            if (left > 0) {
+              acc = over4(acc, c);
+              ++marched;
+              done = (double)acc.w >= a.alpha_stop;
+            }
+            if (!done && left > 1) {
+              acc = over4(acc, odd);
+              ++marched;
+              done = (double)acc.w >= a.alpha_stop;
+            }
+          }
+          done = __shfl_sync(0xffffffffu, done, q) != 0;  // the odd lane follows its pair
+          if (__all_sync(0xffffffffu, done || left <= 2)) break;
+        }
       }
-      stations = parity ? 0u : (uint32_t)n;
+      if constexpr (ET) {
+        if (bad_tail && !done && err && !parity) atomicAdd(err, 1u);  // marched into the bad tail
+        stations = parity ? 0u : marched;
+      } else {
+        stations = parity ? 0u : (uint32_t)n;
+      }
       if (parity || !in_img) {
         warp_stations += stations;
         continue;
@@ -478,8 +521,8 @@ static bool fast_eligible(const isc_render_args* a, FastField& F) {
   if (a->n_sources != 1 || !a->work_counter) return false;
   const isc_source& s = a->src[0];
   if ((s.feature_dim != 1 && s.feature_dim != 3) || s.mode != ISC_VOLUME || s.dtype != ISC_F32) return false;
-  // vector sources: guarded trilinear without early termination (paired path)
-  if (s.feature_dim == 3 && !(a->interpolation && s.has_guard && a->alpha_stop >= 1.0)) return false;
+  // vector sources: guarded trilinear (paired path)
+  if (s.feature_dim == 3 && !(a->interpolation && s.has_guard)) return false;
   const int g = a->guard_width;
   long long ext[3];
   for (int i = 0; i < 3; ++i) ext[i] = a->brick_size[i] + 2LL * g;
@@ -506,7 +549,7 @@ static bool fast_eligible(const isc_render_args* a, FastField& F) {
   return true;
 }
 
-template <bool INTERP, bool GUARDED, bool PAIRED, bool LINE = false, int DIM = 1>
+template <bool INTERP, bool GUARDED, bool PAIRED, bool LINE = false, int DIM = 1, bool ET = false>
 static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_t st) {
   static const int tw_log2 = getenv("ISC_TILE_W") ? __builtin_ctz(atoi(getenv("ISC_TILE_W"))) : 3;
   const int tw = 1 << tw_log2, th = (PAIRED ? 16 : 32) >> tw_log2;
@@ -529,12 +572,13 @@ static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_
   int dev = 0, sms = 148, per_sm = 1;
   ISC_CUDA_CHECK(cudaGetDevice(&dev));
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_fast_kernel<INTERP, GUARDED, PAIRED, LINE, DIM>, kThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_fast_kernel<INTERP, GUARDED, PAIRED, LINE, DIM, ET>, kThreads,
+                                                0);
   const int total_warps = (n_codes + 0);
   int grid = sms * (per_sm > 0 ? per_sm : 1);
   const int need = (total_warps + (kThreads / 32) - 1) / (kThreads / 32);
   if (grid > need) grid = need > 0 ? need : 1;
-  march_fast_kernel<INTERP, GUARDED, PAIRED, LINE, DIM><<<grid, kThreads, 0, st>>>(
+  march_fast_kernel<INTERP, GUARDED, PAIRED, LINE, DIM, ET><<<grid, kThreads, 0, st>>>(
       *a, F, tiles_x, tiles_y, super_x, n_codes, row_order ? 1 : 0, tw_log2, tile_x0, tile_y0);
   ISC_CUDA_CHECK(cudaGetLastError());
   return ISC_OK;
@@ -554,10 +598,18 @@ extern "C" int isc_render_local(const isc_render_args* a, void* stream) {
     const bool guarded = interp && a->src[0].has_guard;
     static const bool no_pair = getenv("ISC_DISABLE_PAIRED") != nullptr;
     const bool paired = !no_pair && a->alpha_stop >= 1.0;
-    if (a->src[0].feature_dim == 3)
-      return a->src[0].lut_linear ? launch_fast<true, true, true, true, 3>(a, F, s)
-                                  : launch_fast<true, true, true, false, 3>(a, F, s);
-    if (interp && guarded && paired && a->src[0].lut_linear) return launch_fast<true, true, true, true>(a, F, s);
+    const bool line = a->src[0].lut_linear != 0;
+    if (a->src[0].feature_dim == 3) {
+      if (a->alpha_stop < 1.0)
+        return line ? launch_fast<true, true, true, true, 3, true>(a, F, s)
+                    : launch_fast<true, true, true, false, 3, true>(a, F, s);
+      return line ? launch_fast<true, true, true, true, 3>(a, F, s) : launch_fast<true, true, true, false, 3>(a, F, s);
+    }
+    // early termination, guarded trilinear: paired with the per-station stop test
+    if (interp && guarded && !no_pair && a->alpha_stop < 1.0)
+      return line ? launch_fast<true, true, true, true, 1, true>(a, F, s)
+                  : launch_fast<true, true, true, false, 1, true>(a, F, s);
+    if (interp && guarded && paired && line) return launch_fast<true, true, true, true>(a, F, s);
     if (interp && guarded) return paired ? launch_fast<true, true, true>(a, F, s) : launch_fast<true, true, false>(a, F, s);
     if (interp) return paired ? launch_fast<true, false, true>(a, F, s) : launch_fast<true, false, false>(a, F, s);
     return paired ? launch_fast<false, false, true>(a, F, s) : launch_fast<false, false, false>(a, F, s);

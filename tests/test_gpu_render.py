@@ -449,3 +449,45 @@ def test_screen_rect_culling_is_exact(multi):
             culled = P.render_local(ctx, scene).pixels.cpu().numpy()
             fullraster = P.render_local(ctx, scene, keep_station_counts=True).pixels.cpu().numpy()
             assert np.array_equal(culled, fullraster), (r, pos)
+
+
+def test_early_termination_stops_before_a_bad_tail():
+    """Early termination on the paired kernel: rays that saturate before the
+    far face of a guard-0 brick gather no bad corner and must not raise; with
+    early termination off the same rays reach the face and must raise
+    (fields.py:230-238: the reference raises only on gathers it performs)."""
+    import math
+    import paper_1611_09048_b200 as P
+    from oracle import isaac_oracle as O
+    torch = _torch()
+    n = 8
+    z, y, x = np.meshgrid(*(np.arange(n, dtype=np.float64),) * 3, indexing="ij")
+    field = (0.6 + 0.05 * np.sin(x + 2 * y + 3 * z)).astype(np.float32)
+    vol = P.GlobalVolume((n, n, n))
+    dom = vol.local_domain(0, 0)
+    cam = dict(position=(-50.0, 3.7, 3.3), look_at=(4.0, 3.7, 3.3), vertical_fov=math.radians(5.0),
+               width=16, height=12)
+    pts = [(0.0, 0.0, 0.0, 0.0, 0.0), (1.0, 1.0, 0.5, 0.2, 1.0)]
+
+    def render(alpha_stop):
+        reg = P.SourceRegistry(dom)
+        reg.register_handle(P.array_backed_handle(P.SourceDescriptor("s", 1, has_guard=True),
+                                                  torch.from_numpy(field).cuda(), 0))
+        P.update_sources(reg, {0}, {})
+        fr = P.default_registry()
+        scene = P.SceneState(
+            camera=P.Camera(cam["position"], cam["look_at"], vertical_fov=cam["vertical_fov"],
+                            image_size=(cam["width"], cam["height"])),
+            tf_points={0: pts}, value_ranges={0: (0.0, 0.7)}, chain_texts={0: ""},
+            settings=P.RenderSettings(active_set=(0,), early_termination_alpha=alpha_stop))
+        img = P.render_local(P.RankContext(vol, dom, reg, fr, fr.limits), scene, keep_station_counts=True)
+        return img.pixels.cpu().numpy(), img.station_counts.cpu().numpy()
+
+    got, counts = render(0.99)
+    ref = O.render_brick(cam, O.Brick((0, 0, 0), (n, n, n), 0, (n, n, n)),
+                         [O.Source(field, (0, 0, 0), (n, n, n), 0, lut=O.lut_from_points(pts), value_range=(0.0, 0.7))],
+                         alpha_stop=0.99)
+    assert np.abs(got - ref.rgba).max() <= 1e-3
+    assert (counts.reshape(-1).astype(np.int64) != ref.stations.reshape(-1)).mean() <= 0.002
+    with pytest.raises(P.GuardContractError):
+        render(1.0)

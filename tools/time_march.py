@@ -20,6 +20,8 @@ def main():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--lut", action="store_true", help="force the shared-memory LUT path")
+    ap.add_argument("--alpha", type=float, default=None, help="early_termination_alpha (default: the config's 1.0)")
+    ap.add_argument("--opacity", type=float, default=None, help="scale the transfer function's alpha ramp")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
     n = cfg["n"]
@@ -37,6 +39,15 @@ def main():
     fr = P.default_registry()
     ctx = P.RankContext(vol, dom, reg, fr, fr.limits)
     scene = bench.build_scene(P, cfg)
+    if args.opacity is not None:
+        pts = {k: [(p[0], p[1], p[2], p[3], p[4] * args.opacity) for p in v] for k, v in scene.tf_points.items()}
+        scene = P.SceneState(camera=scene.camera, tf_points=pts, value_ranges=scene.value_ranges,
+                             chain_texts=scene.chain_texts, clip_planes=scene.clip_planes, settings=scene.settings)
+    if args.alpha is not None:
+        import dataclasses
+        scene = P.SceneState(camera=scene.camera, tf_points=scene.tf_points, value_ranges=scene.value_ranges,
+                             chain_texts=scene.chain_texts, clip_planes=scene.clip_planes,
+                             settings=dataclasses.replace(scene.settings, early_termination_alpha=args.alpha))
     w, h = cfg["image"]
     out = torch.empty((h, w, 4), dtype=torch.float32, device="cuda")
     plans = P.build_plans(reg, fr, fr.limits, scene)
@@ -51,7 +62,8 @@ def main():
         P.render_local(ctx, scene, events=e, **kw)
     torch.cuda.synchronize()
     ms = sorted(a.elapsed_time(b) for a, b in evs)
-    res = {"lib": os.environ.get("ISC_LIB_PATH", "default"), "config": args.config, "median_ms": round(ms[len(ms) // 2], 4),
+    res = {"lib": os.environ.get("ISC_LIB_PATH", "default"), "config": args.config, "alpha": args.alpha,
+           "median_ms": round(ms[len(ms) // 2], 4),
            "min_ms": round(ms[0], 4), "stations": int(img.stations)}
     chk = out.double().sum().item()
     res["checksum"] = round(chk, 3)
