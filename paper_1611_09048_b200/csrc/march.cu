@@ -243,7 +243,8 @@ __device__ __forceinline__ float4 classify_line_premul(const isc_source& s, floa
 #ifndef ISC_FAST_MINB
 #define ISC_FAST_MINB 4  // <= 64 registers: 4 CTAs (32 warps) per SM
 #endif
-template <bool INTERP, bool GUARDED, bool PAIRED, bool LINE = false, int DIM = 1, bool ET = false>
+template <bool INTERP, bool GUARDED, bool PAIRED, bool LINE = false, int DIM = 1, bool ET = false,
+          typename T = float>
 __global__ void __launch_bounds__(kThreads, ISC_FAST_MINB) march_fast_kernel(const __grid_constant__ isc_render_args a,
                                                               const FastField F, int tiles_x, int tiles_y,
                                                               int super_x, int n_codes, int row_order,
@@ -356,13 +357,13 @@ __global__ void __launch_bounds__(kThreads, ISC_FAST_MINB) march_fast_kernel(con
           station_pos(o, r.d, dmul(kd, step), p0);
           float s0;
           if constexpr (DIM == 1) {
-            const float v0 = fast_sample<INTERP, GUARDED, kCheck>(F, p0, err);
+            const float v0 = fast_sample<INTERP, GUARDED, kCheck, T>(F, p0, err);
             float vv[4] = {v0, 0.f, 0.f, 0.f};
             s0 = s.n_steps ? run_chain(s, vv, 1) : v0;
           } else {
             static_assert(INTERP && GUARDED && PAIRED, "vector sources: guarded trilinear paired path only");
             float vv[4] = {0.f, 0.f, 0.f, 0.f};
-            fast_gather<DIM>(F, p0, vv);
+            fast_gather<DIM, T>(F, p0, vv);
             s0 = run_chain_fast<DIM>(s, vv);
           }
           c = LINE ? classify_line_premul(s, lo, inv, s0) : premultiply(classify(lut_s, lo, inv, s0));
@@ -520,7 +521,10 @@ using namespace isc;
 static bool fast_eligible(const isc_render_args* a, FastField& F) {
   if (a->n_sources != 1 || !a->work_counter) return false;
   const isc_source& s = a->src[0];
-  if ((s.feature_dim != 1 && s.feature_dim != 3) || s.mode != ISC_VOLUME || s.dtype != ISC_F32) return false;
+  if ((s.feature_dim != 1 && s.feature_dim != 3) || s.mode != ISC_VOLUME) return false;
+  if (s.dtype != ISC_F32 && !(s.dtype == ISC_F16 || s.dtype == ISC_BF16)) return false;
+  // half-precision fields: scalar, guarded trilinear (paired path)
+  if (s.dtype != ISC_F32 && !(s.feature_dim == 1 && a->interpolation && s.has_guard)) return false;
   // vector sources: guarded trilinear (paired path)
   if (s.feature_dim == 3 && !(a->interpolation && s.has_guard)) return false;
   const int g = a->guard_width;
@@ -535,7 +539,7 @@ static bool fast_eligible(const isc_render_args* a, FastField& F) {
   if (s.stride[3] < 0 || s.stride[3] > INT32_MAX) return false;
   maxoff += (s.feature_dim - 1) * s.stride[3];
   if (maxoff + s.stride[0] + s.stride[1] + s.stride[2] >= INT32_MAX) return false;
-  F.f = reinterpret_cast<const float*>(s.data);
+  F.f = s.data;
   F.sz = (int)s.stride[0];
   F.sy = (int)s.stride[1];
   F.sx = (int)s.stride[2];
@@ -549,7 +553,8 @@ static bool fast_eligible(const isc_render_args* a, FastField& F) {
   return true;
 }
 
-template <bool INTERP, bool GUARDED, bool PAIRED, bool LINE = false, int DIM = 1, bool ET = false>
+template <bool INTERP, bool GUARDED, bool PAIRED, bool LINE = false, int DIM = 1, bool ET = false,
+          typename T = float>
 static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_t st) {
   static const int tw_log2 = getenv("ISC_TILE_W") ? __builtin_ctz(atoi(getenv("ISC_TILE_W"))) : 3;
   const int tw = 1 << tw_log2, th = (PAIRED ? 16 : 32) >> tw_log2;
@@ -572,13 +577,13 @@ static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_
   int dev = 0, sms = 148, per_sm = 1;
   ISC_CUDA_CHECK(cudaGetDevice(&dev));
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_fast_kernel<INTERP, GUARDED, PAIRED, LINE, DIM, ET>, kThreads,
-                                                0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_fast_kernel<INTERP, GUARDED, PAIRED, LINE, DIM, ET, T>,
+                                                kThreads, 0);
   const int total_warps = (n_codes + 0);
   int grid = sms * (per_sm > 0 ? per_sm : 1);
   const int need = (total_warps + (kThreads / 32) - 1) / (kThreads / 32);
   if (grid > need) grid = need > 0 ? need : 1;
-  march_fast_kernel<INTERP, GUARDED, PAIRED, LINE, DIM, ET><<<grid, kThreads, 0, st>>>(
+  march_fast_kernel<INTERP, GUARDED, PAIRED, LINE, DIM, ET, T><<<grid, kThreads, 0, st>>>(
       *a, F, tiles_x, tiles_y, super_x, n_codes, row_order ? 1 : 0, tw_log2, tile_x0, tile_y0);
   ISC_CUDA_CHECK(cudaGetLastError());
   return ISC_OK;
@@ -599,6 +604,19 @@ extern "C" int isc_render_local(const isc_render_args* a, void* stream) {
     static const bool no_pair = getenv("ISC_DISABLE_PAIRED") != nullptr;
     const bool paired = !no_pair && a->alpha_stop >= 1.0;
     const bool line = a->src[0].lut_linear != 0;
+    if (a->src[0].dtype != ISC_F32) {  // __half / __nv_bfloat16 scalar fields (fast_eligible)
+      const bool et = a->alpha_stop < 1.0;
+      if (a->src[0].dtype == ISC_F16) {
+        if (et) return line ? launch_fast<true, true, true, true, 1, true, __half>(a, F, s)
+                            : launch_fast<true, true, true, false, 1, true, __half>(a, F, s);
+        return line ? launch_fast<true, true, true, true, 1, false, __half>(a, F, s)
+                    : launch_fast<true, true, true, false, 1, false, __half>(a, F, s);
+      }
+      if (et) return line ? launch_fast<true, true, true, true, 1, true, __nv_bfloat16>(a, F, s)
+                          : launch_fast<true, true, true, false, 1, true, __nv_bfloat16>(a, F, s);
+      return line ? launch_fast<true, true, true, true, 1, false, __nv_bfloat16>(a, F, s)
+                  : launch_fast<true, true, true, false, 1, false, __nv_bfloat16>(a, F, s);
+    }
     if (a->src[0].feature_dim == 3) {
       if (a->alpha_stop < 1.0)
         return line ? launch_fast<true, true, true, true, 3, true>(a, F, s)

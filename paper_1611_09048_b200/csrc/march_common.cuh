@@ -3,6 +3,9 @@
 // persistent tile scheduler's Morton decode and pair shuffles.
 #pragma once
 
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 #include "raysetup.cuh"
 
@@ -12,7 +15,7 @@ constexpr int kTile = 16;
 constexpr int kThreads = kTile * kTile;
 
 struct FastField {
-  const float* __restrict__ f;
+  const void* __restrict__ f;   // element type: the kernel's T (float, __half, __nv_bfloat16)
   int sx, sy, sz;        // element strides
   int sc;                // component stride (feature_dim > 1)
   int lo[3];             // brick offset - guard (global cell of array index 0)
@@ -41,10 +44,16 @@ __device__ __forceinline__ bool guard_ok(const FastField& F, const double p[3]) 
          (unsigned)(iz - F.lo[2]) <= (unsigned)F.hi[2];
 }
 
+// One field element as float32 (read-only path).
+__device__ __forceinline__ float ldf(const float* p) { return __ldg(p); }
+__device__ __forceinline__ float ldf(const __half* p) { return __half2float(__ldg(p)); }
+__device__ __forceinline__ float ldf(const __nv_bfloat16* p) { return __bfloat162float(__ldg(p)); }
+
 // CHECK = false: the caller has proven the guard contract for this sample
 // (see march_fast_kernel: endpoint check per ray).
-template <bool INTERP, bool GUARDED, bool CHECK = true>
+template <bool INTERP, bool GUARDED, bool CHECK = true, typename T = float>
 __device__ __forceinline__ float fast_sample(const FastField& F, const double p[3], uint32_t* err) {
+  const T* __restrict__ fld = reinterpret_cast<const T*>(F.f);
   int ix, iy, iz;
   const double flx = floor_split(p[0], ix), fly = floor_split(p[1], iy), flz = floor_split(p[2], iz);
   if constexpr (!INTERP) {
@@ -52,7 +61,7 @@ __device__ __forceinline__ float fast_sample(const FastField& F, const double p[
     const int x = min(max(ix - F.lo[0] - F.g, 0), F.hi[0]) + F.g;
     const int y = min(max(iy - F.lo[1] - F.g, 0), F.hi[1]) + F.g;
     const int z = min(max(iz - F.lo[2] - F.g, 0), F.hi[2]) + F.g;
-    return __ldg(F.f + (z * F.sz + y * F.sy + x * F.sx));
+    return ldf(fld + (z * F.sz + y * F.sy + x * F.sx));
   } else {
     const float fx = (float)dsub(p[0], flx), fy = (float)dsub(p[1], fly), fz = (float)dsub(p[2], flz);
     int x0, y0, z0, dx, dy, dz;
@@ -83,10 +92,10 @@ __device__ __forceinline__ float fast_sample(const FastField& F, const double p[
       y0 += F.g;
       z0 += F.g;
     }
-    const float* b = F.f + (z0 * F.sz + y0 * F.sy + x0 * F.sx);
-    const float v000 = __ldg(b), v100 = __ldg(b + dx), v010 = __ldg(b + dy), v110 = __ldg(b + dy + dx);
-    const float* c = b + dz;
-    const float v001 = __ldg(c), v101 = __ldg(c + dx), v011 = __ldg(c + dy), v111 = __ldg(c + dy + dx);
+    const T* b = fld + (z0 * F.sz + y0 * F.sy + x0 * F.sx);
+    const float v000 = ldf(b), v100 = ldf(b + dx), v010 = ldf(b + dy), v110 = ldf(b + dy + dx);
+    const T* c = b + dz;
+    const float v001 = ldf(c), v101 = ldf(c + dx), v011 = ldf(c + dy), v111 = ldf(c + dy + dx);
     const float a0 = fmaf(fx, v100 - v000, v000), a1 = fmaf(fx, v110 - v010, v010);
     const float a2 = fmaf(fx, v101 - v001, v001), a3 = fmaf(fx, v111 - v011, v011);
     const float b0 = fmaf(fy, a1 - a0, a0), b1 = fmaf(fy, a3 - a2, a2);
@@ -96,20 +105,21 @@ __device__ __forceinline__ float fast_sample(const FastField& F, const double p[
 
 // DIM-component trilinear gather with the guard contract already proven for
 // this station (march_fast_kernel's per-ray check): v[c] for c < DIM.
-template <int DIM>
+template <int DIM, typename T = float>
 __device__ __forceinline__ void fast_gather(const FastField& F, const double p[3], float v[4]) {
+  const T* __restrict__ fld = reinterpret_cast<const T*>(F.f);
   int ix, iy, iz;
   const double flx = floor_split(p[0], ix), fly = floor_split(p[1], iy), flz = floor_split(p[2], iz);
   const float fx = (float)dsub(p[0], flx), fy = (float)dsub(p[1], fly), fz = (float)dsub(p[2], flz);
   const int x0 = ix - F.lo[0], y0 = iy - F.lo[1], z0 = iz - F.lo[2];
-  const float* b = F.f + (z0 * F.sz + y0 * F.sy + x0 * F.sx);
+  const T* b = fld + (z0 * F.sz + y0 * F.sy + x0 * F.sx);
   const int dx = F.sx, dy = F.sy, dz = F.sz;
 #pragma unroll
   for (int c = 0; c < DIM; ++c) {
-    const float* q0 = b + c * F.sc;
-    const float v000 = __ldg(q0), v100 = __ldg(q0 + dx), v010 = __ldg(q0 + dy), v110 = __ldg(q0 + dy + dx);
-    const float* q1 = q0 + dz;
-    const float v001 = __ldg(q1), v101 = __ldg(q1 + dx), v011 = __ldg(q1 + dy), v111 = __ldg(q1 + dy + dx);
+    const T* q0 = b + c * F.sc;
+    const float v000 = ldf(q0), v100 = ldf(q0 + dx), v010 = ldf(q0 + dy), v110 = ldf(q0 + dy + dx);
+    const T* q1 = q0 + dz;
+    const float v001 = ldf(q1), v101 = ldf(q1 + dx), v011 = ldf(q1 + dy), v111 = ldf(q1 + dy + dx);
     const float a0 = fmaf(fx, v100 - v000, v000), a1 = fmaf(fx, v110 - v010, v010);
     const float a2 = fmaf(fx, v101 - v001, v001), a3 = fmaf(fx, v111 - v011, v011);
     const float b0 = fmaf(fy, a1 - a0, a0), b1 = fmaf(fy, a3 - a2, a2);

@@ -284,7 +284,9 @@ def _single_source_scene(P, n, pos, look, chain="", tf=None, rng=(0.0, 1.0), act
 
 @pytest.mark.parametrize("dtype", ["float64", "float16", "bfloat16"])
 def test_generic_kernel_other_dtypes(dtype):
-    """Non-float32 fields take the generic kernel (any dtype, 64-bit offsets)."""
+    """Non-float32 fields: float16 / bfloat16 scalars take the paired fast
+    kernel (T = __half / __nv_bfloat16), float64 the generic kernel (any
+    dtype, 64-bit offsets); all against the oracle on the values read."""
     import paper_1611_09048_b200 as P
     from oracle import isaac_oracle as O
     torch = _torch()

@@ -22,12 +22,15 @@ def main():
     ap.add_argument("--lut", action="store_true", help="force the shared-memory LUT path")
     ap.add_argument("--alpha", type=float, default=None, help="early_termination_alpha (default: the config's 1.0)")
     ap.add_argument("--opacity", type=float, default=None, help="scale the transfer function's alpha ramp")
+    ap.add_argument("--dtype", default="float32", help="field element type (float32, float16, bfloat16)")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
     n = cfg["n"]
     vol = P.GlobalVolume((n,) * 3, (1, 1, 1))
     dom = vol.local_domain(0, 1)
     field = bench.make_field_torch(n, dom, "cuda")
+    if args.dtype != "float32":
+        field = field.to(getattr(torch, args.dtype))
     reg = P.SourceRegistry(dom)
     reg.register_handle(P.array_backed_handle(P.SourceDescriptor("density", 1, has_guard=True), field, 1))
     active = {0}
@@ -63,6 +66,7 @@ def main():
     torch.cuda.synchronize()
     ms = sorted(a.elapsed_time(b) for a, b in evs)
     res = {"lib": os.environ.get("ISC_LIB_PATH", "default"), "config": args.config, "alpha": args.alpha,
+           "dtype": args.dtype,
            "median_ms": round(ms[len(ms) // 2], 4),
            "min_ms": round(ms[0], 4), "stations": int(img.stations)}
     chk = out.double().sum().item()
