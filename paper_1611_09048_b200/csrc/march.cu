@@ -522,8 +522,7 @@ static bool fast_eligible(const isc_render_args* a, FastField& F) {
   if (a->n_sources != 1 || !a->work_counter) return false;
   const isc_source& s = a->src[0];
   if ((s.feature_dim != 1 && s.feature_dim != 3) || s.mode != ISC_VOLUME) return false;
-  if (s.dtype != ISC_F32 && !(s.dtype == ISC_F16 || s.dtype == ISC_BF16)) return false;
-  // half-precision fields: scalar, guarded trilinear (paired path)
+  // other element types: scalar, guarded trilinear (paired path)
   if (s.dtype != ISC_F32 && !(s.feature_dim == 1 && a->interpolation && s.has_guard)) return false;
   // vector sources: guarded trilinear (paired path)
   if (s.feature_dim == 3 && !(a->interpolation && s.has_guard)) return false;
@@ -604,8 +603,14 @@ extern "C" int isc_render_local(const isc_render_args* a, void* stream) {
     static const bool no_pair = getenv("ISC_DISABLE_PAIRED") != nullptr;
     const bool paired = !no_pair && a->alpha_stop >= 1.0;
     const bool line = a->src[0].lut_linear != 0;
-    if (a->src[0].dtype != ISC_F32) {  // __half / __nv_bfloat16 scalar fields (fast_eligible)
+    if (a->src[0].dtype != ISC_F32) {  // double / __half / __nv_bfloat16 scalar fields (fast_eligible)
       const bool et = a->alpha_stop < 1.0;
+      if (a->src[0].dtype == ISC_F64) {
+        if (et) return line ? launch_fast<true, true, true, true, 1, true, double>(a, F, s)
+                            : launch_fast<true, true, true, false, 1, true, double>(a, F, s);
+        return line ? launch_fast<true, true, true, true, 1, false, double>(a, F, s)
+                    : launch_fast<true, true, true, false, 1, false, double>(a, F, s);
+      }
       if (a->src[0].dtype == ISC_F16) {
         if (et) return line ? launch_fast<true, true, true, true, 1, true, __half>(a, F, s)
                             : launch_fast<true, true, true, false, 1, true, __half>(a, F, s);

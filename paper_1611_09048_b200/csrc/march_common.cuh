@@ -15,7 +15,7 @@ constexpr int kTile = 16;
 constexpr int kThreads = kTile * kTile;
 
 struct FastField {
-  const void* __restrict__ f;   // element type: the kernel's T (float, __half, __nv_bfloat16)
+  const void* __restrict__ f;   // element type: the kernel's T (float, double, __half, __nv_bfloat16)
   int sx, sy, sz;        // element strides
   int sc;                // component stride (feature_dim > 1)
   int lo[3];             // brick offset - guard (global cell of array index 0)
@@ -48,6 +48,7 @@ __device__ __forceinline__ bool guard_ok(const FastField& F, const double p[3]) 
 __device__ __forceinline__ float ldf(const float* p) { return __ldg(p); }
 __device__ __forceinline__ float ldf(const __half* p) { return __half2float(__ldg(p)); }
 __device__ __forceinline__ float ldf(const __nv_bfloat16* p) { return __bfloat162float(__ldg(p)); }
+__device__ __forceinline__ float ldf(const double* p) { return (float)__ldg(p); }
 
 // CHECK = false: the caller has proven the guard contract for this sample
 // (see march_fast_kernel: endpoint check per ray).

@@ -282,11 +282,13 @@ def _single_source_scene(P, n, pos, look, chain="", tf=None, rng=(0.0, 1.0), act
                         settings=P.RenderSettings(active_set=tuple(active), early_termination_alpha=1.0))
 
 
+@pytest.mark.parametrize("interp", [True, False])
 @pytest.mark.parametrize("dtype", ["float64", "float16", "bfloat16"])
-def test_generic_kernel_other_dtypes(dtype):
-    """Non-float32 fields: float16 / bfloat16 scalars take the paired fast
-    kernel (T = __half / __nv_bfloat16), float64 the generic kernel (any
-    dtype, 64-bit offsets); all against the oracle on the values read."""
+def test_other_dtypes(dtype, interp):
+    """Non-float32 scalar fields: guarded trilinear takes the paired fast
+    kernel with T = double / __half / __nv_bfloat16, nearest the generic
+    any-dtype kernel; checked against the oracle on the values the kernel
+    reads (converted to float32 on load)."""
     import paper_1611_09048_b200 as P
     from oracle import isaac_oracle as O
     torch = _torch()
@@ -304,11 +306,16 @@ def test_generic_kernel_other_dtypes(dtype):
     ctx = P.RankContext(vol, dom, reg, fr, fr.limits)
     pos, look = (31.0, 27.0, -22.0), (10.0, 10.0, 10.0)
     scene = _single_source_scene(P, n, pos, look)
+    if not interp:
+        import dataclasses
+        scene = P.SceneState(camera=scene.camera, tf_points=scene.tf_points, value_ranges=scene.value_ranges,
+                             chain_texts=scene.chain_texts,
+                             settings=dataclasses.replace(scene.settings, interpolation=False))
     got = P.render_local(ctx, scene).pixels.cpu().numpy()
     src = O.Source(array=vals.astype(np.float64), offset=(0, 0, 0), size=(n, n, n), guard=1,
                    lut=O.lut_from_points(scene.tf_points[0]), value_range=(0.0, 1.0))
     ref = O.render_brick({"position": pos, "look_at": look, "width": 48, "height": 32},
-                         O.Brick((0, 0, 0), (n, n, n), 1, (n, n, n)), [src])
+                         O.Brick((0, 0, 0), (n, n, n), 1, (n, n, n)), [src], interp=interp)
     assert np.abs(got - ref.rgba).max() <= RGBA_TOL
 
 
