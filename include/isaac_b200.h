@@ -55,7 +55,7 @@
 extern "C" {
 #endif
 
-#define ISC_ABI_VERSION 1
+#define ISC_ABI_VERSION 2  /* 2: isc_render_args.ray_dirs / ray_intervals, isc_gradient_normals */
 #define ISC_MAX_SOURCES 8      /* active sources per render                 */
 #define ISC_MAX_CLIP_PLANES 8
 #define ISC_MAX_CHAIN 8        /* ChainLimits.max_length default is 5        */

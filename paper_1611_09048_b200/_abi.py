@@ -16,7 +16,7 @@ from . import errors
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("ISC_LIB_PATH") or os.path.join(_HERE, "lib", "libisaac_b200.so")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 MAX_SOURCES = 8
 MAX_CLIP_PLANES = 8
 MAX_CHAIN = 8

@@ -58,6 +58,10 @@ def test_argument_validation_without_device():
     assert lib.isc_render_local(C.byref(a), None) == 1          # FieldError: sizes
     with pytest.raises(_abi.errors.FieldError):
         _abi.check(lib.isc_render_local(C.byref(a), None))
+    a.brick_size[:] = [4, 4, 4]
+    a.volume_size[:] = [4, 4, 4]
+    a.decomposition[:] = [1, 1, 1]
+    assert lib.isc_gradient_normals(C.byref(a), None, None, 1, None, None) == 7   # ValueError: no source in src[0]
     s = _abi.SwapArgs()
     s.size, s.rank, s.n_ctas, s.epoch = 3, 0, 1, 1
     assert lib.isc_binary_swap(C.byref(s), None) == 5           # CompositeError: not a power of two
