@@ -11,6 +11,9 @@
 #include <math_constants.h>
 
 #include <cstdlib>
+#include <cstring>
+#include <deque>
+#include <mutex>
 
 #include "common.cuh"
 #include "march_common.cuh"
@@ -552,6 +555,116 @@ static bool fast_eligible(const isc_render_args* a, FastField& F) {
   return true;
 }
 
+// ---------------------------------------------------------------------------
+// Online occupancy choice for the march kernels.  A region whose rays are
+// far apart (large voxel footprint per pixel, e.g. the far half of a
+// decomposed volume) thrashes L1 with 4 resident CTAs per SM, while the
+// whole C4 volume wants 4 (far half 4.21 ms at 4 CTAs/SM, 2.99
+// at 3; whole volume 4.19 vs 4.77).  The first two renders of a key (field,
+// brick, image, camera, kernel variant) run the two candidates with CUDA
+// events around them; once both have completed (queried without blocking),
+// the faster is kept for that key.  Results are bit-identical either way:
+// only the number of persistent CTAs changes.
+class OccupancyTuner {
+ public:
+  struct Key {
+    const void* data;
+    int dev, variant, w, h, off[3], size[3], n_clip;
+    double origin[3], fwd[3], clip_sig;
+    bool operator==(const Key& o) const { return std::memcmp(this, &o, sizeof(Key)) == 0; }
+  };
+  static Key make_key(const isc_render_args* a, int variant) {
+    Key k;
+    std::memset(&k, 0, sizeof(k));
+    k.data = a->src[0].data;
+    cudaGetDevice(&k.dev);
+    k.variant = variant;
+    k.w = a->camera.width;
+    k.h = a->camera.height;
+    for (int i = 0; i < 3; ++i) {
+      k.off[i] = a->brick_offset[i];
+      k.size[i] = a->brick_size[i];
+      k.origin[i] = a->camera.origin[i];
+      k.fwd[i] = a->camera.fwd[i];
+    }
+    k.n_clip = a->n_clip;  // clip planes change the marched region
+    for (int p = 0; p < a->n_clip; ++p)
+      k.clip_sig += (p + 1) * (a->clip[p].f0 + 3.0 * a->clip[p].normal[0] + 5.0 * a->clip[p].normal[1] +
+                               7.0 * a->clip[p].normal[2]);
+    return k;
+  }
+  // Candidate (CTAs per SM cap, 0 = occupancy maximum) for this launch, and
+  // the events to record around it (null when not a trial).
+  int choose(const Key& k, cudaStream_t st, cudaEvent_t* ev0, cudaEvent_t* ev1) {
+    *ev0 = *ev1 = nullptr;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return 0;
+    std::lock_guard<std::mutex> g(mu_);
+    Entry* e = find(k);
+    if (!e) {
+      if (entries_.size() >= 64) clear_locked();
+      entries_.push_back(Entry{k});
+      e = &entries_.back();
+    }
+    if (e->decided) return e->best;
+    if (e->trials < 2) {
+      const int t = e->trials++;
+      if (cudaEventCreate(&e->ev[t][0]) != cudaSuccess || cudaEventCreate(&e->ev[t][1]) != cudaSuccess) {
+        e->decided = true;
+        e->best = 0;
+        return 0;
+      }
+      *ev0 = e->ev[t][0];
+      *ev1 = e->ev[t][1];
+      return kCandidates[t];
+    }
+    if (cudaEventQuery(e->ev[0][1]) == cudaSuccess && cudaEventQuery(e->ev[1][1]) == cudaSuccess) {
+      float t0 = 0.f, t1 = 0.f;
+      cudaEventElapsedTime(&t0, e->ev[0][0], e->ev[0][1]);
+      cudaEventElapsedTime(&t1, e->ev[1][0], e->ev[1][1]);
+      e->best = t1 < t0 ? kCandidates[1] : kCandidates[0];
+      e->decided = true;
+      release(*e);
+      return e->best;
+    }
+    return kCandidates[0];  // trials still in flight: default, decide on a later call
+  }
+
+ private:
+  static constexpr int kCandidates[2] = {0, 3};
+  struct Entry {
+    Key key;
+    int trials = 0;
+    bool decided = false;
+    int best = 0;
+    cudaEvent_t ev[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  };
+  Entry* find(const Key& k) {
+    for (auto& e : entries_)
+      if (e.key == k) return &e;
+    return nullptr;
+  }
+  static void release(Entry& e) {
+    for (auto& p : e.ev)
+      for (auto& ev : p)
+        if (ev) {
+          cudaEventDestroy(ev);
+          ev = nullptr;
+        }
+  }
+  void clear_locked() {
+    for (auto& e : entries_) release(e);
+    entries_.clear();
+  }
+  std::mutex mu_;
+  std::deque<Entry> entries_;
+};
+
+static OccupancyTuner& tuner() {
+  static OccupancyTuner t;
+  return t;
+}
+
 template <bool INTERP, bool GUARDED, bool PAIRED, bool LINE = false, int DIM = 1, bool ET = false,
           typename T = float>
 static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_t st) {
@@ -576,15 +689,31 @@ static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_
   int dev = 0, sms = 148, per_sm = 1;
   ISC_CUDA_CHECK(cudaGetDevice(&dev));
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static const char* carve = getenv("ISC_CARVEOUT");
+  if (carve)
+    cudaFuncSetAttribute(march_fast_kernel<INTERP, GUARDED, PAIRED, LINE, DIM, ET, T>,
+                         cudaFuncAttributePreferredSharedMemoryCarveout, atoi(carve));
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_fast_kernel<INTERP, GUARDED, PAIRED, LINE, DIM, ET, T>,
                                                 kThreads, 0);
+  static const int cap_env = getenv("ISC_CTAS_PER_SM") ? atoi(getenv("ISC_CTAS_PER_SM")) : 0;
+  static const bool no_tune = getenv("ISC_DISABLE_TUNE") != nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int cap = cap_env;
+  if (!cap && !no_tune && PAIRED) {
+    const int variant = (INTERP ? 1 : 0) | (GUARDED ? 2 : 0) | (LINE ? 4 : 0) | (ET ? 8 : 0) | (DIM << 4) |
+                        ((int)sizeof(T) << 8);
+    cap = tuner().choose(OccupancyTuner::make_key(a, variant), st, &ev0, &ev1);
+  }
+  if (cap > 0 && per_sm > cap) per_sm = cap;
   const int total_warps = (n_codes + 0);
   int grid = sms * (per_sm > 0 ? per_sm : 1);
   const int need = (total_warps + (kThreads / 32) - 1) / (kThreads / 32);
   if (grid > need) grid = need > 0 ? need : 1;
+  if (ev0) cudaEventRecord(ev0, st);
   march_fast_kernel<INTERP, GUARDED, PAIRED, LINE, DIM, ET, T><<<grid, kThreads, 0, st>>>(
       *a, F, tiles_x, tiles_y, super_x, n_codes, row_order ? 1 : 0, tw_log2, tile_x0, tile_y0);
   ISC_CUDA_CHECK(cudaGetLastError());
+  if (ev1) cudaEventRecord(ev1, st);
   return ISC_OK;
 }
 

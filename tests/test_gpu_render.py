@@ -500,3 +500,28 @@ def test_early_termination_stops_before_a_bad_tail():
     assert (counts.reshape(-1).astype(np.int64) != ref.stations.reshape(-1)).mean() <= 0.002
     with pytest.raises(P.GuardContractError):
         render(1.0)
+
+
+def test_occupancy_tuning_is_invisible():
+    """The march kernels' online occupancy choice (two trial launches per
+    key, then the faster) changes only how many persistent CTAs run: every
+    render of a key is bit-identical, before, during and after the trials."""
+    import paper_1611_09048_b200 as P
+    torch = _torch()
+    n = 40
+    rng = np.random.default_rng(23)
+    arr = torch.from_numpy(rng.random((n + 2, n + 2, n + 2)).astype(np.float32)).cuda()
+    vol = P.GlobalVolume((n, n, n))
+    dom = vol.local_domain(0, 1)
+    reg = P.SourceRegistry(dom)
+    reg.register_handle(P.array_backed_handle(P.SourceDescriptor("f", 1, has_guard=True), arr, 1))
+    P.update_sources(reg, {0}, {})
+    fr = P.default_registry()
+    ctx = P.RankContext(vol, dom, reg, fr, fr.limits)
+    scene = _single_source_scene(P, n, (70.0, 55.0, -31.0), (20.0, 20.0, 20.0))
+    imgs = []
+    for _ in range(5):
+        imgs.append(P.render_local(ctx, scene).pixels.cpu().numpy())
+        torch.cuda.synchronize()
+    for im in imgs[1:]:
+        assert np.array_equal(im, imgs[0])
