@@ -560,11 +560,12 @@ static bool fast_eligible(const isc_render_args* a, FastField& F) {
 // far apart (large voxel footprint per pixel, e.g. the far half of a
 // decomposed volume) thrashes L1 with 4 resident CTAs per SM, while the
 // whole C4 volume wants 4 (far half 4.21 ms at 4 CTAs/SM, 2.99
-// at 3; whole volume 4.19 vs 4.77).  The first two renders of a key (field,
-// brick, image, camera, kernel variant) run the two candidates with CUDA
-// events around them; once both have completed (queried without blocking),
-// the faster is kept for that key.  Results are bit-identical either way:
-// only the number of persistent CTAs changes.
+// at 3; whole volume 4.19 vs 4.77).  When a key (field, brick, image,
+// camera, clip planes, kernel variant) is rendered twice in a row (a static
+// view), its next two renders run the two candidates between CUDA events;
+// once both have completed (queried without blocking on a later call) the
+// faster is kept for that key.  Results are bit-identical either way: only
+// the number of persistent CTAs changes.
 class OccupancyTuner {
  public:
   struct Key {
@@ -600,14 +601,20 @@ class OccupancyTuner {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return 0;
     std::lock_guard<std::mutex> g(mu_);
+    // trials only for a key rendered twice in a row (a static view): a
+    // camera sweep (orbit) never pays for trials it cannot reuse
+    const bool repeat = have_last_ && last_ == k;
+    last_ = k;
+    have_last_ = true;
     Entry* e = find(k);
+    if (!e && !repeat) return kCandidates[0];
     if (!e) {
       if (entries_.size() >= 64) clear_locked();
       entries_.push_back(Entry{k});
       e = &entries_.back();
     }
     if (e->decided) return e->best;
-    if (e->trials < 2) {
+    if (e->trials < 2 && repeat) {
       const int t = e->trials++;
       if (cudaEventCreate(&e->ev[t][0]) != cudaSuccess || cudaEventCreate(&e->ev[t][1]) != cudaSuccess) {
         e->decided = true;
@@ -658,6 +665,8 @@ class OccupancyTuner {
   }
   std::mutex mu_;
   std::deque<Entry> entries_;
+  Key last_{};
+  bool have_last_ = false;
 };
 
 static OccupancyTuner& tuner() {
