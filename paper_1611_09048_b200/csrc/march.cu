@@ -698,10 +698,6 @@ static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_
   int dev = 0, sms = 148, per_sm = 1;
   ISC_CUDA_CHECK(cudaGetDevice(&dev));
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  static const char* carve = getenv("ISC_CARVEOUT");
-  if (carve)
-    cudaFuncSetAttribute(march_fast_kernel<INTERP, GUARDED, PAIRED, LINE, DIM, ET, T>,
-                         cudaFuncAttributePreferredSharedMemoryCarveout, atoi(carve));
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_fast_kernel<INTERP, GUARDED, PAIRED, LINE, DIM, ET, T>,
                                                 kThreads, 0);
   static const int cap_env = getenv("ISC_CTAS_PER_SM") ? atoi(getenv("ISC_CTAS_PER_SM")) : 0;
@@ -714,9 +710,8 @@ static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_
     cap = tuner().choose(OccupancyTuner::make_key(a, variant), st, &ev0, &ev1);
   }
   if (cap > 0 && per_sm > cap) per_sm = cap;
-  const int total_warps = (n_codes + 0);
   int grid = sms * (per_sm > 0 ? per_sm : 1);
-  const int need = (total_warps + (kThreads / 32) - 1) / (kThreads / 32);
+  const int need = (n_codes + (kThreads / 32) - 1) / (kThreads / 32);  // one tile per warp at most
   if (grid > need) grid = need > 0 ? need : 1;
   if (ev0) cudaEventRecord(ev0, st);
   march_fast_kernel<INTERP, GUARDED, PAIRED, LINE, DIM, ET, T><<<grid, kThreads, 0, st>>>(
