@@ -252,6 +252,7 @@ def run_b200(args):
     if world > 1:
         host = P.TorchDistTransport()
         transport = P.NvlinkTransport(host, w * h)
+        transport.sync_errors = False     # pipelined frames; checked at flush() below
         canvas = transport.canvas(h, w)
     else:
         transport = P.LocalFabric(1).endpoint(0)
@@ -308,6 +309,8 @@ def run_b200(args):
     end.record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop()
+    if world > 1:
+        transport.flush()             # a timed-out swap raises here
     ms_total = start.elapsed_time(end)
     kernel_ms = sum(a.elapsed_time(b) for a, b in evs) / k
     t = torch.tensor([ms_total, kernel_ms], dtype=torch.float64, device=red_dev)

@@ -243,7 +243,7 @@ def _swap_nvlink(t, pixels, order):
     fn = _abi.lib().isc_binary_swap if (t.size & (t.size - 1)) == 0 else _abi.lib().isc_direct_send
     _abi.check(fn(C.byref(args), C.c_void_p(s)), "binary_swap")
     _account(t, order)
-    t.status(s)
+    t.check_errors(s)
     if t.rank == 0:
         return t.root_output(h, w).clone()
     return None

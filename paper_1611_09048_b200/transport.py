@@ -264,6 +264,11 @@ class NvlinkTransport(_HostCollectives):
     """
 
     timeout_s: float = 30.0
+    # True: every binary_swap synchronises its stream to check the spin-wait
+    # error word (the reference raises from the call).  False: the word is
+    # copied to pinned memory on the stream and checked on a later call or
+    # at flush(), so the host keeps enqueueing frames (pipelined rendering).
+    sync_errors: bool = True
 
     def __init__(self, host=None, n_pixels: int = 0, *, _local=None):
         from . import _abi
@@ -306,6 +311,9 @@ class NvlinkTransport(_HostCollectives):
         self.n_pixels = self.arena.n_pixels
         self.epoch = 0
         self._status_host = torch.zeros(1, dtype=torch.int64).pin_memory()   # allocated up front
+        self._err_slots = [torch.zeros(1, dtype=torch.int64).pin_memory() for _ in range(4)]
+        self._pending: list = []      # (event, slot) of deferred error checks
+        self._next_slot = 0
         sms = _abi.lib().isc_device_sm_count(self.arena.device_index)
         self.n_ctas = max(1, sms if sms > 0 else 148)
         self.sent_bytes = 0
@@ -354,6 +362,50 @@ class NvlinkTransport(_HostCollectives):
                                                         C.c_void_p(self._status_host.data_ptr()), C.byref(code)),
                         "swap status")
         if code.value:
+            raise TransportError(f"rank {self.rank}: peer did not arrive within {self.timeout_s}s "
+                                 "(binary swap spin-wait timed out)")
+
+    def check_errors(self, stream_ptr: int) -> None:
+        """After a swap launch: synchronous check (``sync_errors``) or a
+        deferred one -- the error word is copied into a pinned slot on the
+        stream and examined once that copy has completed."""
+        if self.sync_errors:
+            self.status(stream_ptr)
+            return
+        import torch
+        self._poll(block=len(self._pending) >= len(self._err_slots))
+        slot = self._err_slots[self._next_slot]
+        self._next_slot = (self._next_slot + 1) % len(self._err_slots)
+        stream = torch.cuda.ExternalStream(stream_ptr)
+        with torch.cuda.stream(stream):
+            slot.copy_(self._error_word(), non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+        self._pending.append((ev, slot))
+
+    def flush(self) -> None:
+        """Wait for every deferred error check; raise if a swap timed out."""
+        self._poll(block=True, all_=True)
+
+    def _error_word(self):
+        import torch
+        flags = torch.as_tensor(_CudaArray(self.flags[self.rank], (16,), "<i8"),
+                                device=f"cuda:{self.arena.device_index}")
+        return flags[9:10]
+
+    def _poll(self, block: bool, all_: bool = False) -> None:
+        bad = False
+        while self._pending:
+            ev, slot = self._pending[0]
+            if not ev.query():
+                if not (block or all_):
+                    break
+                ev.synchronize()
+                block = False
+            self._pending.pop(0)
+            bad = bad or int(slot.item()) != 0
+        if bad:
+            self._error_word().zero_()
             raise TransportError(f"rank {self.rank}: peer did not arrive within {self.timeout_s}s "
                                  "(binary swap spin-wait timed out)")
 

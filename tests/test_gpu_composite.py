@@ -137,3 +137,22 @@ def test_multi_process_ipc_swap(name, world):
     assert out.returncode == 0, out.stderr[-3000:]
     res = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
     assert res["max_err"] <= TOL
+
+
+def test_swap_timeout_deferred_check():
+    """sync_errors=False: the swap returns without synchronising; the timed-out
+    spin-wait surfaces as TransportError at flush()."""
+    import torch
+    import paper_1611_09048_b200 as P
+    grp = P.LocalNvlinkGroup(2, 64)
+    try:
+        ep = grp.endpoints[0]
+        ep.timeout_s = 0.2
+        ep.n_ctas = 1
+        ep.sync_errors = False
+        P.binary_swap(ep, torch.zeros((8, 8, 4), device="cuda"), [0, 1])   # rank 1 never arrives
+        with pytest.raises(P.TransportError):
+            ep.flush()
+        ep.flush()   # the error word was cleared: nothing pending
+    finally:
+        grp.close()
