@@ -211,6 +211,7 @@ def run_b200(args):
     import torch.distributed as dist
 
     import paper_1611_09048_b200 as P
+    from paper_1611_09048_b200.raycast import describe_kernel
 
     rank, world, local = dist_env()
     if args.share_gpu:          # test mode: every rank on cuda:0 (ranks time-share one GPU)
@@ -387,7 +388,7 @@ def run_b200(args):
                              else "samples = stations (one active source)"),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "isc::march_fast_kernel<INTERP=1,GUARDED=1,PAIRED=1>", "kernel_ms": round(kernel_ms_max, 4),
+                         "kernel": describe_kernel(plans[0], scenes[0].settings), "kernel_ms": round(kernel_ms_max, 4),
                          "algorithmic_bytes_per_launch": int(br.item() / world)},
             "e2e": e2e,
             "classification": ("analytic single-ramp transfer function (exact: the LUT is one straight run, "

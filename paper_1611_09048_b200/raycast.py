@@ -238,6 +238,34 @@ def _lut_line(lut: np.ndarray, tol: float):
     return base, slope
 
 
+def describe_kernel(plans: Sequence[SourcePlan], settings, analytic_lut: bool = True) -> str:
+    """Name of the march kernel ``isc_render_local`` dispatches to for these
+    plans (mirrors the library's dispatch; for reports and bench lines)."""
+    import torch as _t
+    interp = bool(settings.interpolation)
+    et = settings.early_termination_alpha < 1.0
+    if len(plans) == 1 and plans[0].mode != ISO_MODE:
+        p = plans[0]
+        dim = p.handle.descriptor.feature_dim
+        arr, _ = p.handle.device_view(p.domain)
+        dtype = getattr(arr, "dtype", None)
+        f32 = dtype in (_t.float32, np.float32)
+        guarded = interp and p.handle.descriptor.has_guard
+        line = analytic_lut and lut_line(p.tf.lut) is not None
+        if (dim == 1 and (f32 or guarded)) or (dim == 3 and f32 and guarded):
+            elem = {_t.float32: "float", _t.float64: "double", _t.float16: "__half",
+                    _t.bfloat16: "__nv_bfloat16"}.get(dtype, "float")
+            return (f"isc::march_fast_kernel<INTERP={int(interp)},GUARDED={int(guarded)},PAIRED=1,"
+                    f"LINE={int(line and guarded)},DIM={dim},ET={int(et)},T={elem}>")
+    if 1 <= len(plans) <= 4:
+        dims = [p.handle.descriptor.feature_dim for p in plans]
+        if interp and all(p.handle.descriptor.has_guard for p in plans) and len(plans) <= 2 and \
+                all(d in (1, 3) for d in dims):
+            return f"isc::march_multi_fast_kernel<NS={len(plans)},DIMS={dims}>"
+        return f"isc::march_multi_kernel<NS={len(plans)},INTERP={int(interp)}>"
+    return f"isc::march_kernel<INTERP={int(interp)}>"
+
+
 def render_local(rank_ctx, scene: SceneState, plans: Optional[Sequence[SourcePlan]] = None,
                  station_recorder: Optional[StationRecorder] = None, *, out: Optional[torch.Tensor] = None,
                  stream=None, check_errors: bool = True, keep_station_counts: bool = False,

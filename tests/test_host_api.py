@@ -316,3 +316,27 @@ def test_station_cells_monotone_in_k():
         for a in range(3):
             diff = np.diff(cells[:, a])
             assert (diff >= 0).all() or (diff <= 0).all()
+
+
+def test_describe_kernel_mirrors_dispatch():
+    """Bench lines name the kernel the library dispatches to (host mirror)."""
+    import torch
+    from paper_1611_09048_b200.raycast import build_plans, describe_kernel
+    n = 8
+    dom = P.GlobalVolume((n, n, n)).local_domain(0, 1)
+    reg = P.SourceRegistry(dom)
+    reg.register_handle(P.array_backed_handle(P.SourceDescriptor("s", 1, has_guard=True),
+                                              torch.zeros((n + 2,) * 3), 1))
+    reg.register_handle(P.array_backed_handle(P.SourceDescriptor("v", 3, has_guard=True),
+                                              torch.zeros((n + 2,) * 3 + (3,)), 1))
+    P.update_sources(reg, {0, 1}, {})
+    fr = P.default_registry()
+    linear = [(0.0, 0.0, 0.0, 0.0, 0.0), (1.0, 1.0, 1.0, 1.0, 1.0)]
+    one = P.SceneState(camera=P.Camera((20.0, 17.0, -9.0), (4.0, 4.0, 4.0)), tf_points={0: linear},
+                       settings=P.RenderSettings(active_set=(0,), early_termination_alpha=1.0))
+    k = describe_kernel(build_plans(reg, fr, fr.limits, one), one.settings)
+    assert k.startswith("isc::march_fast_kernel") and "LINE=1" in k and "ET=0" in k
+    two = P.SceneState(camera=one.camera, chain_texts={1: "length"},
+                       settings=P.RenderSettings(active_set=(0, 1), modes={0: "iso"}))
+    assert describe_kernel(build_plans(reg, fr, fr.limits, two), two.settings).startswith(
+        "isc::march_multi_fast_kernel<NS=2")
