@@ -336,6 +336,48 @@ __device__ __forceinline__ bool cell_guard_ok(const MultiField& M, const double 
 // Shaded colour of an iso hit on source si (gradient normal, raycast.py:
 // 210-242, 351-369), out of line so the station loop keeps its registers;
 // direction and position by value so the caller's Ray stays in registers.
+// Rare iso pair tests of source si, out of line (see iso_hit_color): the
+// entry pair's earlier value (station k-1 through the guard) and the forward
+// exit pair (the next brick cannot reach back), raycast.py:384-468.
+__device__ __noinline__ float iso_entry_value(const isc_render_args& a, const MultiField& M, int si, double d0,
+                                              double d1, double d2, int k, uint32_t* err) {
+  const double d[3] = {d0, d1, d2};
+  double off[3], bsz[3], pq[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    off[i] = (double)a.brick_offset[i];
+    bsz[i] = (double)a.brick_size[i];
+  }
+  station_pos(a.camera.origin, d, dmul((double)(k - 1), a.step), pq);
+  return reach(off, bsz, M.g, pq) ? point_scalar<true>(M.s[si], M, a.src[si], pq, err) : CUDART_NAN_F;
+}
+
+__device__ __noinline__ bool iso_exit_pair(const isc_render_args& a, const MultiField& M, int si, double d0,
+                                           double d1, double d2, int k, double p0, double p1, double p2, float sb,
+                                           double* tau, uint32_t* err) {
+  const double d[3] = {d0, d1, d2}, p[3] = {p0, p1, p2};
+  double off[3], bsz[3], vb[3], pn[3], noff[3];
+  station_pos(a.camera.origin, d, dmul((double)(k + 1), a.step), pn);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    off[i] = (double)a.brick_offset[i];
+    bsz[i] = (double)a.brick_size[i];
+    vb[i] = ddiv((double)a.volume_size[i], (double)a.decomposition[i]);  // raycast.py:283-285
+    double c = floor(ddiv(pn[i], vb[i]));
+    c = dmin(dmax(c, 0.0), (double)(a.decomposition[i] - 1));
+    noff[i] = dmul(c, vb[i]);
+  }
+  if (reach(off, bsz, M.g, pn) && !reach(noff, vb, M.g, p)) {
+    const float sn = point_scalar<true>(M.s[si], M, a.src[si], pn, err) - a.src[si].iso_threshold;
+    if ((sb < 0.f) != (sn < 0.f)) {
+      const float den = sb - sn;
+      *tau = den != 0.f ? (double)(sb / den) : 1.0;
+      return true;
+    }
+  }
+  return false;
+}
+
 __device__ __noinline__ float4 iso_hit_color(const isc_render_args& a, const MultiField& M, int si, double d0,
                                              double d1, double d2, double p0, double p1, double p2, double tau,
                                              double back, uint32_t* err) {
@@ -482,16 +524,8 @@ __global__ void __launch_bounds__(kThreads, ISC_MULTI_FAST_MINB)
           const float thr = s.iso_threshold;
           float before = prev[si];
           const int k = (int)kd;
-          if (k == k_lo && k - 1 >= kg_lo) {  // entry pair: sample k-1 through the guard
-            double off[3], bsz[3], pq[3];
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {
-              off[i] = (double)a.brick_offset[i];
-              bsz[i] = (double)a.brick_size[i];
-            }
-            station_pos(o, r.d, dmul((double)(k - 1), step), pq);
-            before = reach(off, bsz, M.g, pq) ? point_scalar<true>(S, M, s, pq, err) : CUDART_NAN_F;
-          }
+          if (k == k_lo && k - 1 >= kg_lo)  // entry pair: sample k-1 through the guard
+            before = iso_entry_value(a, M, si, r.d[0], r.d[1], r.d[2], k, err);
           const float sa = before - thr, sb = cur - thr;
           bool hit = isfinite(sa) && ((sa < 0.f) != (sb < 0.f));
           double tau = 0.0, back = 0.0;
@@ -501,25 +535,11 @@ __global__ void __launch_bounds__(kThreads, ISC_MULTI_FAST_MINB)
             back = -1.0;
           }
           if (!hit && k == k_hi - 1 && k + 1 < kg_hi) {  // exit pair, checked forward
-            double off[3], bsz[3], vb[3], pn[3], noff[3];
-            station_pos(o, r.d, dmul((double)(k + 1), step), pn);
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {
-              off[i] = (double)a.brick_offset[i];
-              bsz[i] = (double)a.brick_size[i];
-              vb[i] = ddiv((double)a.volume_size[i], (double)a.decomposition[i]);  // raycast.py:283-285
-              double c = floor(ddiv(pn[i], vb[i]));
-              c = dmin(dmax(c, 0.0), (double)(a.decomposition[i] - 1));
-              noff[i] = dmul(c, vb[i]);
-            }
-            if (reach(off, bsz, M.g, pn) && !reach(noff, vb, M.g, p)) {
-              const float sn = point_scalar<true>(S, M, s, pn, err) - thr;
-              if ((sb < 0.f) != (sn < 0.f)) {
-                const float den = sb - sn;
-                tau = den != 0.f ? (double)(sb / den) : 1.0;
-                back = 0.0;
-                hit = true;
-              }
+            double tx = 0.0;
+            if (iso_exit_pair(a, M, si, r.d[0], r.d[1], r.d[2], k, p[0], p[1], p[2], sb, &tx, err)) {
+              tau = tx;
+              back = 0.0;
+              hit = true;
             }
           }
           prev[si] = cur;
