@@ -73,7 +73,9 @@ class LutCache:
             if t is not None:
                 self._cache.move_to_end(key)
                 return t
-        t = torch.from_numpy(host).to(device)
+        # pinned staging + stream-ordered copy: a pageable .to(device) would
+        # synchronise the stream and stall the host behind the previous frame
+        t = torch.from_numpy(host).pin_memory().to(device, non_blocking=True)
         with self._lock:
             self.uploads += 1
             self._cache[key] = t
