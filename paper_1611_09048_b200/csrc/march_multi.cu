@@ -147,6 +147,71 @@ __device__ __noinline__ float3 multi_normal(const MultiSrc& S, const MultiField&
   return make_float3(grad[0] / mag, grad[1] / mag, grad[2] / mag);
 }
 
+// Rare iso pair tests of source si, out of line (see iso_hit_color): the
+// entry pair's earlier value (station k-1 through the guard) and the forward
+// exit pair (the next brick cannot reach back), raycast.py:384-468.
+__device__ __noinline__ float iso_entry_value(const isc_render_args& a, const MultiField& M, int si, double d0,
+                                              double d1, double d2, int k, uint32_t* err) {
+  const double d[3] = {d0, d1, d2};
+  double off[3], bsz[3], pq[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    off[i] = (double)a.brick_offset[i];
+    bsz[i] = (double)a.brick_size[i];
+  }
+  station_pos(a.camera.origin, d, dmul((double)(k - 1), a.step), pq);
+  return reach(off, bsz, M.g, pq) ? point_scalar<true>(M.s[si], M, a.src[si], pq, err) : CUDART_NAN_F;
+}
+
+__device__ __noinline__ bool iso_exit_pair(const isc_render_args& a, const MultiField& M, int si, double d0,
+                                           double d1, double d2, int k, double p0, double p1, double p2, float sb,
+                                           double* tau, uint32_t* err) {
+  const double d[3] = {d0, d1, d2}, p[3] = {p0, p1, p2};
+  double off[3], bsz[3], vb[3], pn[3], noff[3];
+  station_pos(a.camera.origin, d, dmul((double)(k + 1), a.step), pn);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    off[i] = (double)a.brick_offset[i];
+    bsz[i] = (double)a.brick_size[i];
+    vb[i] = ddiv((double)a.volume_size[i], (double)a.decomposition[i]);  // raycast.py:283-285
+    double c = floor(ddiv(pn[i], vb[i]));
+    c = dmin(dmax(c, 0.0), (double)(a.decomposition[i] - 1));
+    noff[i] = dmul(c, vb[i]);
+  }
+  if (reach(off, bsz, M.g, pn) && !reach(noff, vb, M.g, p)) {
+    const float sn = point_scalar<true>(M.s[si], M, a.src[si], pn, err) - a.src[si].iso_threshold;
+    if ((sb < 0.f) != (sn < 0.f)) {
+      const float den = sb - sn;
+      *tau = den != 0.f ? (double)(sb / den) : 1.0;
+      return true;
+    }
+  }
+  return false;
+}
+
+template <bool INTERP = true>
+__device__ __noinline__ float4 iso_hit_color(const isc_render_args& a, const MultiField& M, int si, double d0,
+                                             double d1, double d2, double p0, double p1, double p2, double tau,
+                                             double back, uint32_t* err) {
+  const double d[3] = {d0, d1, d2}, p[3] = {p0, p1, p2};
+  const isc_source& s = a.src[si];
+  double hp[3], off[3];
+  int isz[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    off[i] = (double)a.brick_offset[i];
+    isz[i] = a.brick_size[i];
+  }
+  const double tt = dmul(dadd(tau, back), a.step);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) hp[i] = dadd(p[i], dmul(tt, d[i]));
+  const float3 nrm = multi_normal<INTERP>(M.s[si], M, s, off, isz, hp, d, err);
+  const float shade = fabsf(nrm.x * (float)d[0] + nrm.y * (float)d[1] + nrm.z * (float)d[2]);
+  const float4 base = classify(reinterpret_cast<const float4*>(s.lut), s.range_lo, 1.0f / (s.range_hi - s.range_lo),
+                               s.iso_threshold);
+  return make_float4(base.x * shade, base.y * shade, base.z * shade, 1.0f);
+}
+
 template <int NS, bool INTERP, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) march_multi_kernel(const __grid_constant__ isc_render_args a,
                                                                const __grid_constant__ MultiField M, int tiles_x,
@@ -191,6 +256,10 @@ __global__ void __launch_bounds__(kThreads, MINB) march_multi_kernel(const __gri
     setup_ray(a, px, py, r);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     uint32_t stations = 0;
+    int hit_si = -1;                     // first iso source hit (shaded after the loop)
+    long long hit_k = 0;
+    double hit_tau = 0.0, hit_back = 0.0;
+    float4 hit_front = make_float4(0.f, 0.f, 0.f, 0.f);
     if (r.hit) {
       float prev[NS];
 #pragma unroll
@@ -253,22 +322,26 @@ __global__ void __launch_bounds__(kThreads, MINB) march_multi_kernel(const __gri
             }
           }
           prev[si] = cur;
-          if (hit) {
-            double hp[3];
-            const double tt = dmul(dadd(tau, back), step);
-#pragma unroll
-            for (int i = 0; i < 3; ++i) hp[i] = dadd(p[i], dmul(tt, r.d[i]));
-            const double dd[3] = {r.d[0], r.d[1], r.d[2]};  // keeps the Ray out of local memory
-            const float3 n = multi_normal<INTERP>(S, M, s, off, isz, hp, dd, err);
-            const float shade = fabsf(n.x * (float)r.d[0] + n.y * (float)r.d[1] + n.z * (float)r.d[2]);
-            const float4 base = classify(lut, s.range_lo, inv[si], thr);
-            st = over4(st, make_float4(base.x * shade, base.y * shade, base.z * shade, 1.0f));
+          if (hit && !stop) {  // shaded after the loop; later sources sit behind the hit
+            hit_si = si;
+            hit_k = k;
+            hit_tau = tau;
+            hit_back = back;
+            hit_front = st;
             stop = true;
           }
         }
+        if (stop) break;
         acc = over4(acc, st);
-        if (stop || (gate_alpha && (double)acc.w >= a.alpha_stop)) break;
+        if (gate_alpha && (double)acc.w >= a.alpha_stop) break;
       }
+    }
+    if (hit_si >= 0) {  // all hitting lanes of the warp shade together
+      double ph[3];
+      station_pos(o, r.d, dmul((double)hit_k, step), ph);
+      const float4 c = iso_hit_color<INTERP>(a, M, hit_si, r.d[0], r.d[1], r.d[2], ph[0], ph[1], ph[2], hit_tau,
+                                             hit_back, err);
+      acc = over4(acc, over4(hit_front, c));
     }
     const long long pix = (long long)py * a.camera.width + px;
     reinterpret_cast<float4*>(a.out_rgba)[pix] = acc;
@@ -336,70 +409,6 @@ __device__ __forceinline__ bool cell_guard_ok(const MultiField& M, const double 
 // Shaded colour of an iso hit on source si (gradient normal, raycast.py:
 // 210-242, 351-369), out of line so the station loop keeps its registers;
 // direction and position by value so the caller's Ray stays in registers.
-// Rare iso pair tests of source si, out of line (see iso_hit_color): the
-// entry pair's earlier value (station k-1 through the guard) and the forward
-// exit pair (the next brick cannot reach back), raycast.py:384-468.
-__device__ __noinline__ float iso_entry_value(const isc_render_args& a, const MultiField& M, int si, double d0,
-                                              double d1, double d2, int k, uint32_t* err) {
-  const double d[3] = {d0, d1, d2};
-  double off[3], bsz[3], pq[3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    off[i] = (double)a.brick_offset[i];
-    bsz[i] = (double)a.brick_size[i];
-  }
-  station_pos(a.camera.origin, d, dmul((double)(k - 1), a.step), pq);
-  return reach(off, bsz, M.g, pq) ? point_scalar<true>(M.s[si], M, a.src[si], pq, err) : CUDART_NAN_F;
-}
-
-__device__ __noinline__ bool iso_exit_pair(const isc_render_args& a, const MultiField& M, int si, double d0,
-                                           double d1, double d2, int k, double p0, double p1, double p2, float sb,
-                                           double* tau, uint32_t* err) {
-  const double d[3] = {d0, d1, d2}, p[3] = {p0, p1, p2};
-  double off[3], bsz[3], vb[3], pn[3], noff[3];
-  station_pos(a.camera.origin, d, dmul((double)(k + 1), a.step), pn);
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    off[i] = (double)a.brick_offset[i];
-    bsz[i] = (double)a.brick_size[i];
-    vb[i] = ddiv((double)a.volume_size[i], (double)a.decomposition[i]);  // raycast.py:283-285
-    double c = floor(ddiv(pn[i], vb[i]));
-    c = dmin(dmax(c, 0.0), (double)(a.decomposition[i] - 1));
-    noff[i] = dmul(c, vb[i]);
-  }
-  if (reach(off, bsz, M.g, pn) && !reach(noff, vb, M.g, p)) {
-    const float sn = point_scalar<true>(M.s[si], M, a.src[si], pn, err) - a.src[si].iso_threshold;
-    if ((sb < 0.f) != (sn < 0.f)) {
-      const float den = sb - sn;
-      *tau = den != 0.f ? (double)(sb / den) : 1.0;
-      return true;
-    }
-  }
-  return false;
-}
-
-__device__ __noinline__ float4 iso_hit_color(const isc_render_args& a, const MultiField& M, int si, double d0,
-                                             double d1, double d2, double p0, double p1, double p2, double tau,
-                                             double back, uint32_t* err) {
-  const double d[3] = {d0, d1, d2}, p[3] = {p0, p1, p2};
-  const isc_source& s = a.src[si];
-  double hp[3], off[3];
-  int isz[3];
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    off[i] = (double)a.brick_offset[i];
-    isz[i] = a.brick_size[i];
-  }
-  const double tt = dmul(dadd(tau, back), a.step);
-#pragma unroll
-  for (int i = 0; i < 3; ++i) hp[i] = dadd(p[i], dmul(tt, d[i]));
-  const float3 nrm = multi_normal<true>(M.s[si], M, s, off, isz, hp, d, err);
-  const float shade = fabsf(nrm.x * (float)d[0] + nrm.y * (float)d[1] + nrm.z * (float)d[2]);
-  const float4 base = classify(reinterpret_cast<const float4*>(s.lut), s.range_lo, 1.0f / (s.range_hi - s.range_lo),
-                               s.iso_threshold);
-  return make_float4(base.x * shade, base.y * shade, base.z * shade, 1.0f);
-}
-
 #ifndef ISC_MULTI_FAST_MINB
 #define ISC_MULTI_FAST_MINB 2
 #endif
@@ -508,7 +517,6 @@ __global__ void __launch_bounds__(kThreads, ISC_MULTI_FAST_MINB)
 #pragma unroll
         for (int si = 0; si < NS; ++si) {
           const isc_source& s = a.src[si];
-          const MultiSrc& S = M.s[si];
           float cur;
           if (si == 0) cur = run_chain_fast<dim_at<DIMS, 0>()>(s, v[0]);
           else if (si == 1) cur = run_chain_fast<dim_at<DIMS, 1>()>(s, v[1]);
