@@ -113,6 +113,9 @@ __global__ void __launch_bounds__(kThreads) march_kernel(const __grid_constant__
     const bool gate_alpha = a.alpha_stop < 1.0;
     uint32_t* err = a.error_word;
 
+    int hit_si = -1;                     // first iso hit, shaded after the loop
+    double hit_p[3] = {0.0, 0.0, 0.0};
+    float4 hit_front = make_float4(0.f, 0.f, 0.f, 0.f);
     {
       const int ns = a.n_sources;
       float prev[ISC_MAX_SOURCES];
@@ -179,21 +182,28 @@ __global__ void __launch_bounds__(kThreads) march_kernel(const __grid_constant__
             }
           }
           prev[si] = cur;
-          if (hit) {
-            double hp[3];
+          if (hit && !stop) {  // later sources of the station sit behind the opaque hit
             const double t = dmul(dadd(tau, back), a.step);
 #pragma unroll
-            for (int i = 0; i < 3; ++i) hp[i] = dadd(p[i], dmul(t, r.d[i]));
-            const float3 n = iso_normal(s, b, hp, r.d, INTERP, err);
-            const float shade = fabsf(n.x * (float)r.d[0] + n.y * (float)r.d[1] + n.z * (float)r.d[2]);
-            const float4 base = classify(lut, s.range_lo, inv, thr);
-            st = over4(st, make_float4(base.x * shade, base.y * shade, base.z * shade, 1.0f));
+            for (int i = 0; i < 3; ++i) hit_p[i] = dadd(p[i], dmul(t, r.d[i]));
+            hit_si = si;
+            hit_front = st;
             stop = true;
           }
         }
+        if (stop) break;
         acc = over4(acc, st);
-        if (stop || (gate_alpha && (double)acc.w >= a.alpha_stop)) break;
+        if (gate_alpha && (double)acc.w >= a.alpha_stop) break;
       }
+    }
+    if (hit_si >= 0) {  // shaded after the loop: all hitting lanes of the warp together
+      const isc_source& s = a.src[hit_si];
+      const double d[3] = {r.d[0], r.d[1], r.d[2]};
+      const float3 n = iso_normal(s, b, hit_p, d, INTERP, err);
+      const float shade = fabsf(n.x * (float)d[0] + n.y * (float)d[1] + n.z * (float)d[2]);
+      const float4 base = classify(lut_s + hit_si * ISC_LUT_ENTRIES, s.range_lo, 1.0f / (s.range_hi - s.range_lo),
+                                   s.iso_threshold);
+      acc = over4(acc, over4(hit_front, make_float4(base.x * shade, base.y * shade, base.z * shade, 1.0f)));
     }
   }
 
