@@ -75,7 +75,8 @@ class LutCache:
                 return t
         # pinned staging + stream-ordered copy: a pageable .to(device) would
         # synchronise the stream and stall the host behind the previous frame
-        t = torch.from_numpy(host).pin_memory().to(device, non_blocking=True)
+        src = torch.from_numpy(host)
+        t = src.pin_memory().to(device, non_blocking=True) if device.type == "cuda" else src.to(device)
         with self._lock:
             self.uploads += 1
             self._cache[key] = t
