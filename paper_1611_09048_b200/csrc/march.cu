@@ -566,16 +566,18 @@ static bool fast_eligible(const isc_render_args* a, FastField& F) {
 }
 
 // ---------------------------------------------------------------------------
-// Online occupancy choice for the march kernels.  A region whose rays are
+// Online launch-shape choice for the paired march.  A region whose rays are
 // far apart (large voxel footprint per pixel, e.g. the far half of a
-// decomposed volume) thrashes L1 with 4 resident CTAs per SM, while the
-// whole C4 volume wants 4 (far half 4.21 ms at 4 CTAs/SM, 2.99
-// at 3; whole volume 4.19 vs 4.77).  When a key (field, brick, image,
-// camera, clip planes, kernel variant) is rendered twice in a row (a static
-// view), its next two renders run the two candidates between CUDA events;
-// once both have completed (queried without blocking on a later call) the
-// faster is kept for that key.  Results are bit-identical either way: only
-// the number of persistent CTAs changes.
+// decomposed volume) thrashes L1 with 4 resident CTAs per SM and prefers a
+// squarer warp tile, while the whole C4 volume wants 4 CTAs and 8x2 tiles
+// (far half 4.21 ms at (4, 8x2), 2.92 at (3, 8x2), 2.57 at
+// (3, 4x4); whole volume 4.19 / 4.77 / 4.85).  When a key (field, brick,
+// image, camera, clip planes, kernel variant) is rendered twice in a row (a
+// static view), its next renders run the candidates between CUDA events --
+// (4, 8x2) and (3, 8x2), then (3, 4x4) only if 3 CTAs won -- and once a
+// stage's trials have completed (queried without blocking on a later call)
+// the fastest is kept.  Results are bit-identical for every choice: only the
+// number of persistent CTAs and the ray-to-lane layout change.
 class OccupancyTuner {
  public:
   struct Key {
@@ -604,12 +606,18 @@ class OccupancyTuner {
                                7.0 * a->clip[p].normal[2]);
     return k;
   }
-  // Candidate (CTAs per SM cap, 0 = occupancy maximum) for this launch, and
-  // the events to record around it (null when not a trial).
-  int choose(const Key& k, cudaStream_t st, cudaEvent_t* ev0, cudaEvent_t* ev1) {
+  // Launch configuration: CTAs-per-SM cap (0 = occupancy maximum) and warp
+  // tile width (log2; 3 = 8x2 rays, 2 = 4x4).
+  struct Choice {
+    int cap, tw_log2;
+  };
+  // Staged search per key: trial A = (max, 8x2), trial B = (3, 8x2); if B
+  // wins (the region is L1-bound), trial C = (3, 4x4).  Returns this launch's
+  // choice and the events to record around it (null when not a trial).
+  Choice choose(const Key& k, cudaStream_t st, cudaEvent_t* ev0, cudaEvent_t* ev1) {
     *ev0 = *ev1 = nullptr;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return 0;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return kCand[0];
     std::lock_guard<std::mutex> g(mu_);
     // trials only for a key rendered twice in a row (a static view): a
     // camera sweep (orbit) never pays for trials it cannot reuse
@@ -617,45 +625,59 @@ class OccupancyTuner {
     last_ = k;
     have_last_ = true;
     Entry* e = find(k);
-    if (!e && !repeat) return kCandidates[0];
+    if (!e && !repeat) return kCand[0];
     if (!e) {
       if (entries_.size() >= 64) clear_locked();
       entries_.push_back(Entry{k});
       e = &entries_.back();
     }
     if (e->decided) return e->best;
-    if (e->trials < 2 && repeat) {
-      const int t = e->trials++;
+    // finish the stage whose trials have all completed
+    if (e->trials == e->planned && done(*e)) {
+      float t[3] = {0.f, 0.f, 0.f};
+      for (int i = 0; i < e->planned; ++i) cudaEventElapsedTime(&t[i], e->ev[i][0], e->ev[i][1]);
+      int best = 0;
+      for (int i = 1; i < e->planned; ++i)
+        if (t[i] < t[best]) best = i;
+      if (e->planned == 2 && best == 1) {
+        e->planned = 3;  // L1-bound region: also try the squarer warp tile
+      } else {
+        e->best = kCand[best];
+        e->decided = true;
+        release(*e);
+        return e->best;
+      }
+    }
+    if (e->trials < e->planned && repeat) {
+      const int t = e->trials;
       if (cudaEventCreate(&e->ev[t][0]) != cudaSuccess || cudaEventCreate(&e->ev[t][1]) != cudaSuccess) {
         e->decided = true;
-        e->best = 0;
-        return 0;
+        e->best = kCand[0];
+        return kCand[0];
       }
+      ++e->trials;
       *ev0 = e->ev[t][0];
       *ev1 = e->ev[t][1];
-      return kCandidates[t];
+      return kCand[t];
     }
-    if (cudaEventQuery(e->ev[0][1]) == cudaSuccess && cudaEventQuery(e->ev[1][1]) == cudaSuccess) {
-      float t0 = 0.f, t1 = 0.f;
-      cudaEventElapsedTime(&t0, e->ev[0][0], e->ev[0][1]);
-      cudaEventElapsedTime(&t1, e->ev[1][0], e->ev[1][1]);
-      e->best = t1 < t0 ? kCandidates[1] : kCandidates[0];
-      e->decided = true;
-      release(*e);
-      return e->best;
-    }
-    return kCandidates[0];  // trials still in flight: default, decide on a later call
+    return kCand[0];  // trials in flight: the default, decide on a later call
   }
 
  private:
-  static constexpr int kCandidates[2] = {0, 3};
+  static constexpr Choice kCand[3] = {{0, 3}, {3, 3}, {3, 2}};
   struct Entry {
     Key key;
     int trials = 0;
+    int planned = 2;
     bool decided = false;
-    int best = 0;
-    cudaEvent_t ev[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+    Choice best = {0, 3};
+    cudaEvent_t ev[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
   };
+  static bool done(const Entry& e) {
+    for (int i = 0; i < e.planned; ++i)
+      if (cudaEventQuery(e.ev[i][1]) != cudaSuccess) return false;
+    return true;
+  }
   Entry* find(const Key& k) {
     for (auto& e : entries_)
       if (e.key == k) return &e;
@@ -687,7 +709,17 @@ static OccupancyTuner& tuner() {
 template <bool INTERP, bool GUARDED, bool PAIRED, bool LINE = false, int DIM = 1, bool ET = false,
           typename T = float>
 static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_t st) {
-  static const int tw_log2 = getenv("ISC_TILE_W") ? __builtin_ctz(atoi(getenv("ISC_TILE_W"))) : 3;
+  static const int tw_env = getenv("ISC_TILE_W") ? __builtin_ctz(atoi(getenv("ISC_TILE_W"))) : -1;
+  static const int cap_env = getenv("ISC_CTAS_PER_SM") ? atoi(getenv("ISC_CTAS_PER_SM")) : 0;
+  static const bool no_tune = getenv("ISC_DISABLE_TUNE") != nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  OccupancyTuner::Choice ch{cap_env, tw_env >= 0 ? tw_env : 3};
+  if (!cap_env && tw_env < 0 && !no_tune && PAIRED) {
+    const int variant = (INTERP ? 1 : 0) | (GUARDED ? 2 : 0) | (LINE ? 4 : 0) | (ET ? 8 : 0) | (DIM << 4) |
+                        ((int)sizeof(T) << 8);
+    ch = tuner().choose(OccupancyTuner::make_key(a, variant), st, &ev0, &ev1);
+  }
+  const int tw_log2 = ch.tw_log2;
   const int tw = 1 << tw_log2, th = (PAIRED ? 16 : 32) >> tw_log2;
   int tiles_x = (a->camera.width + tw - 1) / tw, tiles_y = (a->camera.height + th - 1) / th;
   int tile_x0 = 0, tile_y0 = 0;
@@ -710,16 +742,7 @@ static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_fast_kernel<INTERP, GUARDED, PAIRED, LINE, DIM, ET, T>,
                                                 kThreads, 0);
-  static const int cap_env = getenv("ISC_CTAS_PER_SM") ? atoi(getenv("ISC_CTAS_PER_SM")) : 0;
-  static const bool no_tune = getenv("ISC_DISABLE_TUNE") != nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  int cap = cap_env;
-  if (!cap && !no_tune && PAIRED) {
-    const int variant = (INTERP ? 1 : 0) | (GUARDED ? 2 : 0) | (LINE ? 4 : 0) | (ET ? 8 : 0) | (DIM << 4) |
-                        ((int)sizeof(T) << 8);
-    cap = tuner().choose(OccupancyTuner::make_key(a, variant), st, &ev0, &ev1);
-  }
-  if (cap > 0 && per_sm > cap) per_sm = cap;
+  if (ch.cap > 0 && per_sm > ch.cap) per_sm = ch.cap;
   int grid = sms * (per_sm > 0 ? per_sm : 1);
   const int need = (n_codes + (kThreads / 32) - 1) / (kThreads / 32);  // one tile per warp at most
   if (grid > need) grid = need > 0 ? need : 1;

@@ -51,8 +51,9 @@ def main():
         fr = P.default_registry()
         ctx = P.RankContext(vol, dom, reg, fr, fr.limits)
         plans = P.build_plans(reg, fr, fr.limits, scene)
-        for _ in range(3):      # three: the library's occupancy choice needs a repeat + two trials
+        for _ in range(5):      # the library's launch-shape choice: a repeat + up to three trials
             img = P.render_local(ctx, scene, plans=plans, out=out, check_errors=False)
+            torch.cuda.synchronize()
         torch.cuda.synchronize()
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.reps)]
         for e in evs:
