@@ -641,6 +641,7 @@ class OccupancyTuner {
         if (t[i] < t[best]) best = i;
       if (e->planned == 2 && best == 1) {
         e->planned = 3;  // L1-bound region: also try the squarer warp tile
+        e->provisional = kCand[1];
       } else {
         e->best = kCand[best];
         e->decided = true;
@@ -660,7 +661,7 @@ class OccupancyTuner {
       *ev1 = e->ev[t][1];
       return kCand[t];
     }
-    return kCand[0];  // trials in flight: the default, decide on a later call
+    return e->provisional;  // trials in flight: best known so far, decide on a later call
   }
 
  private:
@@ -671,6 +672,7 @@ class OccupancyTuner {
     int planned = 2;
     bool decided = false;
     Choice best = {0, 3};
+    Choice provisional = {0, 3};
     cudaEvent_t ev[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
   };
   static bool done(const Entry& e) {
