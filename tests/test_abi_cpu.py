@@ -72,3 +72,15 @@ def test_product_path_fails_loudly_without_library(monkeypatch, tmp_path):
     monkeypatch.setattr(_abi, "LIB_PATH", str(tmp_path / "missing.so"))
     with pytest.raises(_abi.NativeLibraryMissing):
         _abi.lib()
+
+
+def test_integration_stub_matches_library():
+    """The ctypes stub a reference maintainer would paste
+    has the library's struct layouts and ABI version."""
+    if not os.path.exists(_abi.LIB_PATH):
+        pytest.skip("library not built")
+    with open(os.path.join(ROOT, "INTEGRATION.md")) as fh:
+        text = fh.read()
+    code = text[text.index("class ChainStep"):text.index("# inside the reference's render_local")]
+    ns = {"C": C, "lib": C.CDLL(_abi.LIB_PATH)}
+    exec(code, ns)     # runs the stub's own asserts (version, struct sizes)
