@@ -20,6 +20,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 import threading
+import weakref
 from dataclasses import dataclass
 from typing import Callable, Optional, Sequence
 
@@ -205,6 +206,60 @@ def pack_render_args(domain, volume, scene: SceneState, plans: Sequence[SourcePl
     return a
 
 
+class _ArgsCache:
+    """Packed launch blocks of recent (scene, plans, domain, volume) objects.
+    A frame that re-renders the same immutable scene objects (a static view,
+    the bench loop) reuses the 3 KB block instead of re-packing it; every
+    reuse re-validates what the block points at: each source's device array
+    (pointer, shape, strides, dtype, guard) and each transfer function's LUT
+    bytes.  Entries hold only weak references to the key objects (an ``id``
+    reused by a new object fails the identity check) and strong references to
+    the LUT tensors the block points at -- never to simulation fields.
+    Sources staged per frame (numpy, host samplers) are never cached."""
+
+    def __init__(self, capacity: int = 16):
+        self._entries: "dict" = {}
+        self._lock = threading.Lock()
+        self.capacity = capacity
+
+    @staticmethod
+    def _fingerprint(plans, domain):
+        fp, fields = [], []
+        for plan in plans:
+            array, guard = plan.handle.device_view(domain)
+            if not (isinstance(array, torch.Tensor) and array.is_cuda):
+                return None, None
+            fp.append((array.data_ptr(), tuple(array.shape), tuple(array.stride()), array.dtype, guard,
+                       hash(np.ascontiguousarray(plan.tf.lut).tobytes())))
+            fields.append(array)
+        return tuple(fp), fields
+
+    def get(self, key, objects, plans, domain):
+        with self._lock:
+            e = self._entries.get(key)
+        if e is None or any(r() is not o for r, o in zip(e[3], objects)):
+            return None
+        fp, fields = self._fingerprint(plans, domain)
+        if fp is None or fp != e[1]:
+            return None
+        return _abi.RenderArgs.from_buffer_copy(e[0]), list(e[2]) + fields
+
+    def put(self, key, objects, plans, domain, args, keep):
+        fp, _ = self._fingerprint(plans, domain)
+        if fp is None:
+            return
+        try:
+            refs = [weakref.ref(o) for o in objects]
+        except TypeError:
+            return
+        luts = [t for t in keep if t.dtype == torch.float32 and tuple(t.shape) == (_abi.LUT_ENTRIES, 4)]
+        with self._lock:
+            if len(self._entries) >= self.capacity:
+                self._entries.pop(next(iter(self._entries)))
+            self._entries[key] = (bytes(args), fp, luts, refs)
+
+
+_ARGS = _ArgsCache()
 _LINE_CACHE: dict = {}
 _LINE_LOCK = threading.Lock()
 
@@ -286,7 +341,15 @@ def render_local(rank_ctx, scene: SceneState, plans: Optional[Sequence[SourcePla
         plans = build_plans(rank_ctx.registry, rank_ctx.functor_registry, rank_ctx.limits, scene)
     w, h = scene.camera.image_size
     keep: list = []
-    args = pack_render_args(domain, volume, scene, plans, device, keep, analytic_lut)
+    objects = (scene, *plans, domain, volume)
+    key = (tuple(id(o) for o in objects), analytic_lut, device.index)
+    hit = _ARGS.get(key, objects, plans, domain)
+    if hit is not None:
+        args, kept = hit
+        keep.extend(kept)
+    else:
+        args = pack_render_args(domain, volume, scene, plans, device, keep, analytic_lut)
+        _ARGS.put(key, objects, plans, domain, args, keep)
     if out is None:
         out = torch.empty((h, w, 4), dtype=torch.float32, device=device)
     elif out.shape != (h, w, 4) or out.dtype != torch.float32 or not out.is_contiguous() or out.device != device:

@@ -567,3 +567,37 @@ def test_random_cameras_bricks_early_termination_vs_oracle():
             err = np.abs(got - ref.rgba).max(axis=-1)
             # early termination: a float32 threshold test may end a ray one station apart
             assert (err > RGBA_TOL).mean() <= (0.002 if alpha_stop < 1.0 else 0.0), (trial, r, err.max())
+
+
+def test_launch_block_cache_revalidates():
+    """Re-rendering the same scene objects reuses the packed launch block, but
+    a different field tensor behind the same handle (update_sources swapping
+    arrays) or a steered transfer function is picked up: images match fresh
+    renders."""
+    import paper_1611_09048_b200 as P
+    torch = _torch()
+    n = 16
+    rng = np.random.default_rng(31)
+    a0 = torch.from_numpy(rng.random((n + 2,) * 3).astype(np.float32)).cuda()
+    a1 = torch.from_numpy(rng.random((n + 2,) * 3).astype(np.float32)).cuda()
+    vol = P.GlobalVolume((n, n, n))
+    dom = vol.local_domain(0, 1)
+    reg = P.SourceRegistry(dom)
+    h = P.array_backed_handle(P.SourceDescriptor("f", 1, has_guard=True), a0, 1)
+    reg.register_handle(h)
+    P.update_sources(reg, {0}, {})
+    fr = P.default_registry()
+    ctx = P.RankContext(vol, dom, reg, fr, fr.limits)
+    scene = _single_source_scene(P, n, (40.0, 30.0, -20.0), (8.0, 8.0, 8.0))
+    plans = P.build_plans(reg, fr, fr.limits, scene)
+    first = P.render_local(ctx, scene, plans=plans).pixels.cpu().numpy()
+    again = P.render_local(ctx, scene, plans=plans).pixels.cpu().numpy()
+    assert np.array_equal(first, again)
+    h.array = a1                                   # the simulation swapped its buffer
+    swapped = P.render_local(ctx, scene, plans=plans).pixels.cpu().numpy()
+    h2 = P.array_backed_handle(P.SourceDescriptor("g", 1, has_guard=True), a1, 1)
+    reg2 = P.SourceRegistry(dom)
+    reg2.register_handle(h2)
+    P.update_sources(reg2, {0}, {})
+    fresh = P.render_local(P.RankContext(vol, dom, reg2, fr, fr.limits), scene).pixels.cpu().numpy()
+    assert np.array_equal(swapped, fresh) and not np.array_equal(swapped, first)
