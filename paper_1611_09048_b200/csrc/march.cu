@@ -11,11 +11,9 @@
 #include <math_constants.h>
 
 #include <cstdlib>
-#include <cstring>
-#include <deque>
-#include <mutex>
 
 #include "common.cuh"
+#include "launch_tuner.cuh"
 #include "march_common.cuh"
 #include "raysetup.cuh"
 #include "sample.cuh"
@@ -565,148 +563,6 @@ static bool fast_eligible(const isc_render_args* a, FastField& F) {
   return true;
 }
 
-// ---------------------------------------------------------------------------
-// Online launch-shape choice for the paired march.  A region whose rays are
-// far apart (large voxel footprint per pixel, e.g. the far half of a
-// decomposed volume) thrashes L1 with 4 resident CTAs per SM and prefers a
-// squarer warp tile, while the whole C4 volume wants 4 CTAs and 8x2 tiles
-// (far half 4.21 ms at (4, 8x2), 2.92 at (3, 8x2), 2.57 at
-// (3, 4x4); whole volume 4.19 / 4.77 / 4.85).  When a key (field, brick,
-// image, camera, clip planes, kernel variant) is rendered twice in a row (a
-// static view), its next renders run the candidates between CUDA events --
-// (4, 8x2) and (3, 8x2), then (3, 4x4) only if 3 CTAs won -- and once a
-// stage's trials have completed (queried without blocking on a later call)
-// the fastest is kept.  Results are bit-identical for every choice: only the
-// number of persistent CTAs and the ray-to-lane layout change.
-class OccupancyTuner {
- public:
-  struct Key {
-    const void* data;
-    int dev, variant, w, h, off[3], size[3], n_clip;
-    double origin[3], fwd[3], clip_sig;
-    bool operator==(const Key& o) const { return std::memcmp(this, &o, sizeof(Key)) == 0; }
-  };
-  static Key make_key(const isc_render_args* a, int variant) {
-    Key k;
-    std::memset(&k, 0, sizeof(k));
-    k.data = a->src[0].data;
-    cudaGetDevice(&k.dev);
-    k.variant = variant;
-    k.w = a->camera.width;
-    k.h = a->camera.height;
-    for (int i = 0; i < 3; ++i) {
-      k.off[i] = a->brick_offset[i];
-      k.size[i] = a->brick_size[i];
-      k.origin[i] = a->camera.origin[i];
-      k.fwd[i] = a->camera.fwd[i];
-    }
-    k.n_clip = a->n_clip;  // clip planes change the marched region
-    for (int p = 0; p < a->n_clip; ++p)
-      k.clip_sig += (p + 1) * (a->clip[p].f0 + 3.0 * a->clip[p].normal[0] + 5.0 * a->clip[p].normal[1] +
-                               7.0 * a->clip[p].normal[2]);
-    return k;
-  }
-  // Launch configuration: CTAs-per-SM cap (0 = occupancy maximum) and warp
-  // tile width (log2; 3 = 8x2 rays, 2 = 4x4).
-  struct Choice {
-    int cap, tw_log2;
-  };
-  // Staged search per key: trial A = (max, 8x2), trial B = (3, 8x2); if B
-  // wins (the region is L1-bound), trial C = (3, 4x4).  Returns this launch's
-  // choice and the events to record around it (null when not a trial).
-  Choice choose(const Key& k, cudaStream_t st, cudaEvent_t* ev0, cudaEvent_t* ev1) {
-    *ev0 = *ev1 = nullptr;
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return kCand[0];
-    std::lock_guard<std::mutex> g(mu_);
-    // trials only for a key rendered twice in a row (a static view): a
-    // camera sweep (orbit) never pays for trials it cannot reuse
-    const bool repeat = have_last_ && last_ == k;
-    last_ = k;
-    have_last_ = true;
-    Entry* e = find(k);
-    if (!e && !repeat) return kCand[0];
-    if (!e) {
-      if (entries_.size() >= 64) clear_locked();
-      entries_.push_back(Entry{k});
-      e = &entries_.back();
-    }
-    if (e->decided) return e->best;
-    // finish the stage whose trials have all completed
-    if (e->trials == e->planned && done(*e)) {
-      float t[3] = {0.f, 0.f, 0.f};
-      for (int i = 0; i < e->planned; ++i) cudaEventElapsedTime(&t[i], e->ev[i][0], e->ev[i][1]);
-      int best = 0;
-      for (int i = 1; i < e->planned; ++i)
-        if (t[i] < t[best]) best = i;
-      if (e->planned == 2 && best == 1) {
-        e->planned = 3;  // L1-bound region: also try the squarer warp tile
-        e->provisional = kCand[1];
-      } else {
-        e->best = kCand[best];
-        e->decided = true;
-        release(*e);
-        return e->best;
-      }
-    }
-    if (e->trials < e->planned && repeat) {
-      const int t = e->trials;
-      if (cudaEventCreate(&e->ev[t][0]) != cudaSuccess || cudaEventCreate(&e->ev[t][1]) != cudaSuccess) {
-        e->decided = true;
-        e->best = kCand[0];
-        return kCand[0];
-      }
-      ++e->trials;
-      *ev0 = e->ev[t][0];
-      *ev1 = e->ev[t][1];
-      return kCand[t];
-    }
-    return e->provisional;  // trials in flight: best known so far, decide on a later call
-  }
-
- private:
-  static constexpr Choice kCand[3] = {{0, 3}, {3, 3}, {3, 2}};
-  struct Entry {
-    Key key;
-    int trials = 0;
-    int planned = 2;
-    bool decided = false;
-    Choice best = {0, 3};
-    Choice provisional = {0, 3};
-    cudaEvent_t ev[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
-  };
-  static bool done(const Entry& e) {
-    for (int i = 0; i < e.planned; ++i)
-      if (cudaEventQuery(e.ev[i][1]) != cudaSuccess) return false;
-    return true;
-  }
-  Entry* find(const Key& k) {
-    for (auto& e : entries_)
-      if (e.key == k) return &e;
-    return nullptr;
-  }
-  static void release(Entry& e) {
-    for (auto& p : e.ev)
-      for (auto& ev : p)
-        if (ev) {
-          cudaEventDestroy(ev);
-          ev = nullptr;
-        }
-  }
-  void clear_locked() {
-    for (auto& e : entries_) release(e);
-    entries_.clear();
-  }
-  std::mutex mu_;
-  std::deque<Entry> entries_;
-  Key last_{};
-  bool have_last_ = false;
-};
-
-static OccupancyTuner& tuner() {
-  static OccupancyTuner t;
-  return t;
-}
 
 template <bool INTERP, bool GUARDED, bool PAIRED, bool LINE = false, int DIM = 1, bool ET = false,
           typename T = float>
