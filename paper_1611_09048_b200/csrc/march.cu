@@ -2,12 +2,19 @@
 // brick.  Replaces raycast.render_local (raycast.py:492-541) together with
 // march_rays (291-381), _iso_detect (384-468) and gradient_normals (210-242).
 //
-// Execution model: one thread per pixel, 16x16 pixel tile per CTA, each warp
-// an 8x4 sub-tile so the 32 rays of a warp stay spatially coherent and their
-// trilinear gathers share L1 lines.  Positions, cell indices and fractions
-// are float64 (bit-identical cell selection to the reference); field values,
-// chains, classification and the over-accumulation are float32.  The
-// transfer-function LUTs of all active sources live in shared memory.
+// Kernels and dispatch (isc_render_local):
+//   march_fast_kernel   one volume-mode source (f32 scalar or float3, f64 /
+//                       f16 / bf16 scalar): persistent warps pull tiles of
+//                       8x2 rays (or 4x4, launch_tuner.cuh), lanes l and
+//                       l + 16 march the even / odd stations of one ray;
+//                       guard contract proven per ray; optional analytic
+//                       single-ramp classification and early termination
+//   march_multi_*       1-4 float32 sources incl. iso surfaces (march_multi.cu)
+//   march_kernel        generic fallback: any dtype, up to 8 sources, static
+//                       16x16-pixel CTAs (8x4 rays per warp)
+// Positions, cell indices and fractions are float64 (bit-identical cell
+// selection to the reference); field values, chains, classification and the
+// over-accumulation are float32.
 #include <math_constants.h>
 
 #include <cstdlib>
