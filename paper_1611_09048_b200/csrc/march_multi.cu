@@ -416,7 +416,8 @@ __device__ __forceinline__ bool cell_guard_ok(const MultiField& M, const double 
 template <int NS, int DIMS>
 __global__ void __launch_bounds__(kThreads, ISC_MULTI_FAST_MINB)
     march_multi_fast_kernel(const __grid_constant__ isc_render_args a, const __grid_constant__ MultiField M,
-                            int tiles_x, int tiles_y, int super_x, int n_codes, int tile_x0, int tile_y0) {
+                            int tiles_x, int tiles_y, int super_x, int n_codes, int tile_x0, int tile_y0,
+                            int tw_log2) {
   __shared__ float4 lut_s[NS * ISC_LUT_ENTRIES];
   for (int i = threadIdx.x; i < NS * ISC_LUT_ENTRIES; i += blockDim.x)
     lut_s[i] = reinterpret_cast<const float4*>(a.src[i >> 8].lut)[i & (ISC_LUT_ENTRIES - 1)];
@@ -441,7 +442,8 @@ __global__ void __launch_bounds__(kThreads, ISC_MULTI_FAST_MINB)
     const int tx = (sblk % super_x) * 8 + morton3(w, 0);
     const int ty = (sblk / super_x) * 8 + morton3(w, 1);
     if (tx >= tiles_x || ty >= tiles_y) continue;
-    const int px = (tx + tile_x0) * 8 + (lane & 7), py = (ty + tile_y0) * 4 + (lane >> 3);
+    const int px = ((tx + tile_x0) << tw_log2) + (lane & ((1 << tw_log2) - 1));
+    const int py = (ty + tile_y0) * (32 >> tw_log2) + (lane >> tw_log2);
     if (px >= a.camera.width || py >= a.camera.height) continue;
 
     Ray r;
@@ -594,16 +596,18 @@ __global__ void __launch_bounds__(kThreads, ISC_MULTI_FAST_MINB)
 
 template <int NS, int DIMS>
 static int launch_multi_fast(const isc_render_args* a, const MultiField& M, cudaStream_t st) {
-  int tiles_x = (a->camera.width + 7) / 8, tiles_y = (a->camera.height + 3) / 4;
+  static const int tw_log2 = getenv("ISC_MULTI_TILE_W") ? __builtin_ctz(atoi(getenv("ISC_MULTI_TILE_W"))) : 3;
+  const int tw = 1 << tw_log2, th = 32 >> tw_log2;
+  int tiles_x = (a->camera.width + tw - 1) / tw, tiles_y = (a->camera.height + th - 1) / th;
   int tile_x0 = 0, tile_y0 = 0;
   int rx0, ry0, rx1, ry1;
   static const bool no_cull = getenv("ISC_DISABLE_CULL") != nullptr;
   if (!no_cull && brick_screen_rect(a, rx0, ry0, rx1, ry1)) {  // see march.cu launch_fast
     ISC_CUDA_CHECK(cudaMemsetAsync(a->out_rgba, 0, (size_t)a->camera.width * a->camera.height * sizeof(float4), st));
-    tile_x0 = rx0 / 8;
-    tile_y0 = ry0 / 4;
-    tiles_x = rx1 > rx0 ? (rx1 + 7) / 8 - tile_x0 : 0;
-    tiles_y = ry1 > ry0 ? (ry1 + 3) / 4 - tile_y0 : 0;
+    tile_x0 = rx0 / tw;
+    tile_y0 = ry0 / th;
+    tiles_x = rx1 > rx0 ? (rx1 + tw - 1) / tw - tile_x0 : 0;
+    tiles_y = ry1 > ry0 ? (ry1 + th - 1) / th - tile_y0 : 0;
     if (tiles_x == 0 || tiles_y == 0) return ISC_OK;
   }
   const int super_x = (tiles_x + 7) / 8, super_y = (tiles_y + 7) / 8;
@@ -616,7 +620,7 @@ static int launch_multi_fast(const isc_render_args* a, const MultiField& M, cuda
   const int need = (n_codes + (kThreads / 32) - 1) / (kThreads / 32);
   if (grid > need) grid = need > 0 ? need : 1;
   march_multi_fast_kernel<NS, DIMS><<<grid, kThreads, 0, st>>>(*a, M, tiles_x, tiles_y, super_x, n_codes, tile_x0,
-                                                                tile_y0);
+                                                                tile_y0, tw_log2);
   ISC_CUDA_CHECK(cudaGetLastError());
   return ISC_OK;
 }
