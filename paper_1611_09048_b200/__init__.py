@@ -31,7 +31,7 @@ def __getattr__(name):
         from . import compositing
         return getattr(compositing, name)
     if name in ("FrameStreamer", "broadcast_scene", "encode_frame", "decode_frame", "frame_pipeline",
-                "merge_metadata", "to_rgba8", "PipelineContext"):
+                "merge_metadata", "to_rgba8", "PipelineContext", "FrameGraph"):
         from . import runtime
         return getattr(runtime, name)
     if name in ("value_range", "auto_value_ranges"):

@@ -63,8 +63,12 @@ class OccupancyTuner {
   Choice choose(const Key& k, cudaStream_t st, cudaEvent_t* ev0, cudaEvent_t* ev1) {
     *ev0 = *ev1 = nullptr;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return kCand[0];
+    const bool capturing = cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone;
     std::lock_guard<std::mutex> g(mu_);
+    if (capturing) {  // a CUDA graph bakes in the launch: the decided (or best known) shape, no trials
+      Entry* e = find(k);
+      return e ? (e->decided ? e->best : e->provisional) : kCand[0];
+    }
     // trials only for a key rendered twice in a row (a static view): a
     // camera sweep (orbit) never pays for trials it cannot reuse
     const bool repeat = have_last_ && last_ == k;

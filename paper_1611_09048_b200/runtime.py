@@ -264,3 +264,48 @@ def frame_pipeline(ctx: PipelineContext, frame_payload: dict) -> Optional[FrameR
         if ctx.streamer is not None:
             ctx.streamer.submit(full, step, metadata, scene)
     return FrameResult(step, full if ctx.is_root else None, metadata, controls, render_s, comp_s, image.stations)
+
+
+class FrameGraph:
+    """A static view's frame (``render_local`` + ``binary_swap``) captured once
+    as a CUDA graph and replayed per frame -- no host preparation, one graph
+    launch.  For one rank (``LocalFabric`` of size 1 / no transport): the
+    peer-memory swap's epoch handshake is host state and cannot be replayed.
+
+    The fields are read in place at replay time (zero-copy, as every render);
+    the scene, plans, transfer functions and the brick's device arrays must
+    stay the ones captured.  ``replay()`` returns the frame tensor, which the
+    next replay overwrites (``frame`` is that same tensor).
+    """
+
+    def __init__(self, rank_ctx, scene: SceneState, warmup: int = 4):
+        import torch
+        from .raycast import build_plans, render_local
+        tr = rank_ctx.transport
+        if tr is not None and getattr(tr, "size", 1) != 1:
+            raise ValueError("FrameGraph replays one rank's frame; multi-rank swaps are not replayable")
+        self.plans = build_plans(rank_ctx.registry, rank_ctx.functor_registry, rank_ctx.limits, scene)
+        w, h = scene.camera.image_size
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.canvas = torch.empty((h, w, 4), dtype=torch.float32, device=dev)
+        order = visibility_order(rank_ctx.global_volume, scene.camera)
+        self._stream = torch.cuda.Stream()
+
+        def frame():
+            img = render_local(rank_ctx, scene, plans=self.plans, out=self.canvas, check_errors=False)
+            self._last = img
+            return binary_swap(tr, img.pixels, order) if tr is not None else img.pixels.clone()
+
+        # warm-up on the capture stream: LUT uploads, launch block, launch-shape choice
+        with torch.cuda.stream(self._stream):
+            for _ in range(warmup):
+                frame()
+                self._stream.synchronize()
+        self._last.check()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self._stream):
+            self.frame = frame()
+
+    def replay(self):
+        self.graph.replay()
+        return self.frame
