@@ -20,6 +20,7 @@ so no explicit L2 flush is needed between steps (stated in ``config``).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import os
@@ -153,6 +154,8 @@ class ClockSampler:
         self.path = os.path.join("/tmp", f"isc_clocks_{os.getpid()}.csv")
 
     def start(self):
+        if os.environ.get("ISC_BENCH_NO_CLOCKS"):   # experiment switch: no sampler
+            return
         try:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
@@ -303,12 +306,18 @@ def run_b200(args):
     barrier()
     clocks.start()
     time.sleep(0.3)
+    # Python's cyclic GC off for the timed steps (as timeit does): a full
+    # collection over torch's object graph can pause the enqueueing host for
+    # tens of ms, i.e. idle the GPU inside the timed region
+    gc.collect()
+    gc.disable()
     barrier()
     start.record(stream)
     for i in range(k):
         step(evs[i])
     end.record(stream)
     torch.cuda.synchronize()
+    gc.enable()
     clk = clocks.stop()
     if world > 1:
         transport.flush()             # a timed-out swap raises here
@@ -535,12 +544,15 @@ def run_e2e(P, torch, dist, ctx, scene, transport, canvas, order, rank, world, r
         dist.barrier()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
+    gc.collect()
+    gc.disable()                    # as in the device-timed loop
     t0.record(stream)
     for _ in range(steps):
         one()
     stream.wait_stream(copy_stream)
     t1.record(stream)
     torch.cuda.synchronize()
+    gc.enable()
     ms = t0.elapsed_time(t1)
     tt = torch.tensor([ms], dtype=torch.float64, device=red_dev)
     if world > 1:

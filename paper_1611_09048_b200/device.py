@@ -59,11 +59,36 @@ class LutCache:
     """Device float32 LUTs keyed by content, so an unchanged transfer function
     is uploaded once and steering changes cost one 4 KB H2D copy."""
 
+    _SLOTS = 8
+
     def __init__(self, capacity: int = 64):
         self._cache: "OrderedDict[tuple, torch.Tensor]" = OrderedDict()
         self._lock = threading.Lock()       # rank threads share one cache
         self.capacity = capacity
         self.uploads = 0
+        self._staging = None                # pinned slots + the events of their last copies
+        self._slot = 0
+
+    def _upload(self, host: np.ndarray, device: torch.device) -> torch.Tensor:
+        """Stream-ordered H2D copy through a ring of pinned staging slots (no
+        stream synchronisation, no pinned allocation per upload)."""
+        if device.type != "cuda" or host.shape != (256, 4):
+            return torch.from_numpy(host).to(device)
+        with self._lock:
+            if self._staging is None:
+                self._staging = [[torch.empty((256, 4), dtype=torch.float32).pin_memory(), None]
+                                 for _ in range(self._SLOTS)]
+            slot = self._staging[self._slot]
+            self._slot = (self._slot + 1) % self._SLOTS
+            if slot[1] is not None:
+                slot[1].synchronize()       # that slot's previous copy (8 uploads ago)
+            slot[0].numpy()[:] = host
+            dev = torch.empty((256, 4), dtype=torch.float32, device=device)
+            dev.copy_(slot[0], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            slot[1] = ev
+        return dev
 
     def get(self, lut: np.ndarray, device: torch.device) -> torch.Tensor:
         host = np.ascontiguousarray(lut, dtype=np.float32)
@@ -75,8 +100,7 @@ class LutCache:
                 return t
         # pinned staging + stream-ordered copy: a pageable .to(device) would
         # synchronise the stream and stall the host behind the previous frame
-        src = torch.from_numpy(host)
-        t = src.pin_memory().to(device, non_blocking=True) if device.type == "cuda" else src.to(device)
+        t = self._upload(host, device)
         with self._lock:
             self.uploads += 1
             self._cache[key] = t

@@ -375,7 +375,7 @@ def render_local(rank_ctx, scene: SceneState, plans: Optional[Sequence[SourcePla
     img._stations = lambda: int(stats[0].item())
     taps = 8 if scene.settings.interpolation else 1
     for plan in plans:
-        plan.handle.add_device_samples(lambda img=img, taps=taps: taps * img.stations)
+        plan.handle.add_device_samples(stats[0], taps)
     img.station_counts = counts
     img.krange = kr
     if check_errors:
@@ -483,7 +483,7 @@ def march_rays(origin, dirs, local_interval, global_interval, plans: Sequence[So
     stations = int(stats[0].item())
     taps = 8 if settings.interpolation else 1
     for plan in plans:
-        plan.handle.add_device_samples(lambda st=stations, taps=taps: taps * st)
+        plan.handle.add_device_samples(stations, taps)
     return out.reshape(n, 4).double().cpu().numpy(), stations
 
 
