@@ -266,11 +266,15 @@ def run_b200(args):
     stream = torch.cuda.current_stream()
     counter = [0]
 
-    def step(events=None):
+    def step(events=None, swap_events=None):
         i = counter[0] % len(scenes)
         counter[0] += 1
         img = P.render_local(ctx, scenes[i], plans=plans[i], out=canvas, check_errors=False, events=events)
+        if swap_events is not None:
+            swap_events[0].record(stream)
         full = P.binary_swap(transport, img.pixels, orders[i])
+        if swap_events is not None:
+            swap_events[1].record(stream)
         return img, full
 
     def barrier():
@@ -302,6 +306,7 @@ def run_b200(args):
     clocks = ClockSampler(local)
     k = args.steps
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
+    sevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     clocks.start()
@@ -314,7 +319,7 @@ def run_b200(args):
     barrier()
     start.record(stream)
     for i in range(k):
-        step(evs[i])
+        step(evs[i], sevs[i])
     end.record(stream)
     torch.cuda.synchronize()
     gc.enable()
@@ -323,10 +328,29 @@ def run_b200(args):
         transport.flush()             # a timed-out swap raises here
     ms_total = start.elapsed_time(end)
     kernel_ms = sum(a.elapsed_time(b) for a, b in evs) / k
+    swap_ms = sum(a.elapsed_time(b) for a, b in sevs) / k
     t = torch.tensor([ms_total, kernel_ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total, kernel_ms_max = float(t[0]), float(t[1])
+    # compositing: per-rank time of the binary_swap call (spin-waits for late
+    # partners included); its minimum over ranks is the last-arriving rank's,
+    # i.e. transfer + over without waiting.  Each rank pulls / stores n*16 B
+    # through peer memory per frame in a binary swap (rank 0 reads (R-1)*n*16 B
+    # in a direct send).
+    composite = None
+    if world > 1:
+        sw = torch.tensor([swap_ms, -swap_ms], dtype=torch.float64, device=red_dev)
+        dist.all_reduce(sw, op=dist.ReduceOp.MAX)
+        swap_max, swap_min = float(sw[0]), -float(sw[1])
+        pow2 = (world & (world - 1)) == 0
+        peer_bytes = w * h * 16 * (1 if pow2 else (world - 1))
+        composite = {"kind": "binary_swap" if pow2 else "direct_send", "ms_max_over_ranks": round(swap_max, 4),
+                     "ms_min_over_ranks": round(swap_min, 4),
+                     "share_of_frame": round(swap_min / (ms_total / k), 4),
+                     "peer_bytes_per_rank": peer_bytes,
+                     "peer_GBps": round(peer_bytes / (swap_min * 1e-3) / 1e9, 1) if swap_min > 0 else None,
+                     "note": "min over ranks = the last-arriving rank's swap (no waiting): transfer + over"}
     ms_step = ms_total / k
     fps = 1000.0 / ms_step
     gsps = samples_frame * fps / 1e9
@@ -422,6 +446,7 @@ def run_b200(args):
                                "'lut_path'") if lut_path else "shared-memory LUT",
             "lut_path": lut_path,
             "graph_replay": graph_replay,
+            "composite": composite,
             "e2e_host_field": host_field,
             "normalisation": norm,
             "gpu_launches": k * (1 + (1 if world > 1 else 0)),
