@@ -33,7 +33,24 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "frames/sec and Gsamples/sec at 1024³×1080p, 1/2/4/8 B200; % of HBM roofline"
-DECOMP = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2), 16: (4, 2, 2)}
+def decomposition(world):
+    """Bricks per axis for `world` ranks: powers of two split x, y, z in turn
+    (1x1x1, 2x1x1, 2x2x1, 2x2x2, 4x2x2, ...); other counts put their prime
+    factors, largest first, on the currently smallest axis."""
+    d = [1, 1, 1]
+    n, p, primes = world, 2, []
+    while n > 1:
+        while n % p == 0:
+            primes.append(p)
+            n //= p
+        p += 1
+    for f in sorted(primes, reverse=True) if world & (world - 1) else primes:
+        a = d.index(min(d))
+        d[a] *= f
+    return tuple(d)
+
+
+DECOMP = {n: decomposition(n) for n in range(1, 65)}
 CONFIGS = {
     "c4": dict(n=1024, image=(1920, 1080), desc="1024^3 float32 field (1 cell guard), 1920x1080, trilinear, "
                                                 "linear TF, harness camera, step 0.5, bricks across N GPUs"),
@@ -217,7 +234,10 @@ def run_b200(args):
     from paper_1611_09048_b200.raycast import describe_kernel
 
     rank, world, local = dist_env()
-    if args.share_gpu:          # test mode: every rank on cuda:0 (ranks time-share one GPU)
+    if world > torch.cuda.device_count() and not args.share_gpu:
+        raise SystemExit(f"bench: {world} ranks but only {torch.cuda.device_count()} visible GPU(s); "
+                         "use --share-gpu for a one-GPU rehearsal")
+    if args.share_gpu:          # rehearsal: every rank on cuda:0 (ranks time-share one GPU)
         local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -230,7 +250,10 @@ def run_b200(args):
     cfg = CONFIGS[args.config]
     w, h = cfg["image"]
     decomp = DECOMP[world]
-    size = tuple(cfg["n"] * decomp[a] for a in range(3)) if cfg.get("weak") else (cfg["n"],) * 3
+    if cfg.get("weak"):
+        size = tuple(cfg["n"] * decomp[a] for a in range(3))
+    else:   # strong scaling; a non-power-of-two rank count trims the volume to divide evenly
+        size = tuple(cfg["n"] - cfg["n"] % decomp[a] for a in range(3))
     n = size[0]
     volume = P.GlobalVolume(size, decomp)
     domain = volume.local_domain(rank, 1)
@@ -432,7 +455,8 @@ def run_b200(args):
                        "volume": list(size), "image": [w, h], "decomposition": list(decomp),
                        "samples_per_frame": samples_frame, "field_bytes_per_gpu": field.numel() * 4,
                        "l2": "inputs larger than L2 (field >> 126 MB); no flush needed",
-                       "parallelism": f"bricks{decomp[0]}x{decomp[1]}x{decomp[2]}"},
+                       "parallelism": f"bricks{decomp[0]}x{decomp[1]}x{decomp[2]}",
+                       "ranks_share_one_gpu": bool(args.share_gpu and world > 1)},
             "gsamples_per_s": round(gsps, 3),
             "samples_note": ("samples = stations x active sources; iso rays stop at the hit" if cfg.get("multi")
                              else "samples = stations (one active source)"),
@@ -743,14 +767,57 @@ def main():
     ap.add_argument("--ref-step-s", type=float, default=4.0)
     ap.add_argument("--share-gpu", action="store_true", help="test only: all ranks on cuda:0")
     ap.add_argument("--no-host-field-e2e", action="store_true")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch the ranks, form the process group (gloo), report the world and exit")
     args = ap.parse_args()
     if args.warmup < 3:
         log("note: warmup < 3 requested; using 3")
         args.warmup = 3
-    if args.impl == "reference":
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "b200":
+        sys.exit(relaunch(args.gpus))
+    _, world, _ = dist_env()
+    if args.impl == "b200" and world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but the launcher started {world} rank(s)")
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_b200(args)
+
+
+def relaunch(n):
+    """``python bench.py --gpus N`` outside torchrun: start N ranks (one
+    process per GPU) with torch.distributed.run on 127.0.0.1 and return its
+    exit code; rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    log(f"bench: launching {n} ranks: {' '.join(cmd)}")
+    return subprocess.call(cmd)
+
+
+def run_dry(args):
+    """Launcher check without a GPU: every rank joins a gloo group and rank 0
+    reports how many ranks answered and the brick each would render."""
+    import torch
+    import torch.distributed as dist
+    rank, world, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    t = torch.tensor([1.0, float(rank)])
+    if world > 1:
+        dist.all_reduce(t)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ranks_seen": int(t[0].item()),
+                          "rank_sum": int(t[1].item()), "decomposition": list(DECOMP[world])}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -55,7 +55,9 @@
 extern "C" {
 #endif
 
-#define ISC_ABI_VERSION 2  /* 2: isc_render_args.ray_dirs / ray_intervals, isc_gradient_normals */
+#define ISC_ABI_VERSION 3  /* 2: isc_render_args.ray_dirs / ray_intervals, isc_gradient_normals;
+                              3: per-slice swap counters, isc_swap_reset, isc_debug_occupy,
+                                 isc_render_args.no_layout */
 #define ISC_MAX_SOURCES 8      /* active sources per render                 */
 #define ISC_MAX_CLIP_PLANES 8
 #define ISC_MAX_CHAIN 8        /* ChainLimits.max_length default is 5        */
@@ -63,6 +65,8 @@ extern "C" {
 #define ISC_MAX_RANKS 64
 #define ISC_MAX_ROUNDS 6       /* log2(ISC_MAX_RANKS)                         */
 #define ISC_IPC_HANDLE_BYTES 64
+#define ISC_MAX_SWAP_CTAS 1024 /* slices (= CTAs) of one swap launch        */
+#define ISC_SWAP_STAGES 9      /* per-slice counters: ready, rounds, collect, root read */
 
 typedef enum {
   ISC_OK = 0,
@@ -171,6 +175,11 @@ typedef struct {
    * [ceil(max(t0,0)/step), ceil(max(t1,0)/step)).  Null in a frame render. */
   const double* ray_dirs;
   const double* ray_intervals;
+  /* 1 = no volume layout (march_rays(volume=None), raycast.py:396-418): an
+   * iso entry pair of a guarded trilinear source samples station k-1 clamped
+   * into [offset-g, offset+size+g-1-1e-9] instead of testing reachability,
+   * and no exit pairs are checked.  0 in a frame render. */
+  int32_t no_layout;
 } isc_render_args;
 /* isc_render_local zeroes *error_word, *out_station_total and *work_counter
  * (stream-ordered) before the march, so callers never need a separate fill. */
@@ -211,17 +220,22 @@ ISC_API int isc_over(float* dst, const float* front, const float* back, int64_t 
 ISC_API int isc_composite_fold(float* out, const float* const* images, int32_t n_images,
                        int64_t n_pixels, void* stream);
 
-/* Binary swap over peer memory.  Every rank runs one persistent kernel; in
- * round r it pulls its partner's half-span straight out of the partner's
- * image (NVLink peer load), composites it with its own half in visibility
- * order and writes it in place; after the last round every rank stores its
- * 1/R span directly into rank 0's output.  Cross-GPU ordering uses
- * epoch-tagged arrival counters in each rank's flag block (no host round
- * trips).  Pointers for other ranks are peer-mapped (isc_ipc_open) or, for
- * ranks sharing one device, plain device pointers. */
+/* Binary swap over peer memory.  Every rank runs one persistent kernel of
+ * n_ctas CTAs; the image is cut into n_ctas contiguous slices and CTA b runs
+ * the reference's binary swap on slice b: in round r it pulls its partner's
+ * half of the slice-b span straight out of the partner's image (NVLink peer
+ * load), composites it with its own half in visibility order and writes it
+ * in place; after the last round it stores its final span directly into
+ * rank 0's output.  Per pixel the tree of `over`s is the reference's, so
+ * results are bit-identical to a whole-image swap.  Ordering uses
+ * epoch-tagged per-slice arrival counters in each rank's flag block (no host
+ * round trips, no grid-wide barrier: the grid need not be co-resident).
+ * n_ctas and n_pixels must be equal on every rank.  Pointers for other ranks
+ * are peer-mapped (isc_ipc_open) or, for ranks sharing one device, plain
+ * device pointers. */
 typedef struct {
   int32_t rank, size;            /* this rank, world size (power of two) */
-  int32_t n_ctas;                /* fixed grid of the exchange kernel    */
+  int32_t n_ctas;                /* slices = CTAs, same on every rank    */
   int32_t round_begin, round_end;/* rounds executed by this launch       */
   int32_t collect;               /* 1: store final span into root_out    */
   int32_t finish;                /* 1: wait until peers stopped reading  */
@@ -241,6 +255,17 @@ ISC_API int isc_flag_words(void);
  * `pinned` (page-locked host memory owned by the caller), then a stream sync. */
 ISC_API int isc_swap_status(unsigned long long* flags, void* stream, unsigned long long* pinned,
                             int32_t* out_code);
+
+/* Stream-ordered copy of the error word into `pinned` (no synchronisation):
+ * the deferred form of isc_swap_status, read once the stream passed it. */
+ISC_API int isc_swap_error_async(unsigned long long* flags, unsigned long long* pinned, void* stream);
+/* Zero a rank's flag block (stream-ordered).  Collective recovery after a
+ * TransportError: every rank resets its own block, then all restart at epoch 1. */
+ISC_API int isc_swap_reset(unsigned long long* flags, void* stream);
+/* Test aid: occupy the GPU with n_ctas CTAs of `threads` threads that spin
+ * for `ns` nanoseconds (a stand-in for the simulation's kernels sharing the
+ * GPU with the compositor). */
+ISC_API int isc_debug_occupy(int32_t n_ctas, int32_t threads, int64_t ns, void* stream);
 
 /* Direct-send fallback for non-power-of-two world sizes: rank 0 folds every
  * rank's image (peer loads) in visibility order into root_out; other ranks

@@ -16,13 +16,15 @@ from . import errors
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("ISC_LIB_PATH") or os.path.join(_HERE, "lib", "libisaac_b200.so")
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 MAX_SOURCES = 8
 MAX_CLIP_PLANES = 8
 MAX_CHAIN = 8
 LUT_ENTRIES = 256
 MAX_RANKS = 64
 IPC_HANDLE_BYTES = 64
+MAX_SWAP_CTAS = 1024
+ERR_WORD = 9          # transport error word of a flag block (composite.cu kErrWord)
 
 F32, F64, F16, BF16 = 0, 1, 2, 3
 VOLUME, ISO = 0, 1
@@ -98,6 +100,7 @@ class RenderArgs(C.Structure):
         ("work_counter", C.c_void_p),
         ("ray_dirs", C.c_void_p),
         ("ray_intervals", C.c_void_p),
+        ("no_layout", C.c_int32),
     ]
 
 
@@ -156,6 +159,9 @@ _SIGNATURES = {
     "isc_direct_send": (C.c_int, [C.POINTER(SwapArgs), C.c_void_p]),
     "isc_flag_words": (C.c_int, []),
     "isc_swap_status": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int32)]),
+    "isc_swap_reset": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "isc_swap_error_async": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "isc_debug_occupy": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, C.c_void_p]),
     "isc_arena_alloc": (C.c_int, [C.c_size_t, C.POINTER(C.c_void_p)]),
     "isc_arena_free": (C.c_int, [C.c_void_p]),
     "isc_ipc_handle": (C.c_int, [C.c_void_p, C.c_char * IPC_HANDLE_BYTES]),

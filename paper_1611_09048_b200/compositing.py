@@ -259,6 +259,8 @@ def binary_swap_local(group, images, order):
     order = list(order)
     eps = group.endpoints
     size = group.size
+    if len({ep.n_ctas for ep in eps}) != 1:
+        raise CompositeError("every rank must cut the image into the same number of slices (n_ctas)")
     shape = tuple(images[0].shape)
     h, w = shape[0], shape[1]
     for r, ep in enumerate(eps):

@@ -10,21 +10,47 @@
 // peer-mapped pointer (NVLink 5 loads on a multi-GPU box), composites it with
 // the local half in visibility order and writes the result in place, so the
 // transfer and the `over` are the same instruction stream.  After the last
-// round each rank stores its 1/R span directly into rank 0's output (the
-// collection step of compositing.py:169-181).  Ranks order themselves through
-// epoch-tagged arrival counters living in each rank's flag block: a CTA
-// publishes "stage s done" with a system-scope release add, a reader spins on
-// a system-scope acquire load of its peer's counter (bounded by a timeout so a
-// missing peer surfaces as TransportError instead of a hung GPU).
+// round each rank stores its final span directly into rank 0's output (the
+// collection step of compositing.py:169-181).
+//
+// Slices.  The image is cut into n_ctas contiguous slices and CTA b of every
+// rank runs the reference's binary swap on slice b alone: round r halves the
+// slice-b span at (lo+hi)/2 and keeps the high half iff bit r of the rank's
+// visibility position is set, exactly as compositing.py:145-160 does on the
+// whole image.  Every pixel therefore sees the same tree of `over`s as the
+// reference (bit-identical results); only which rank holds which pixels at
+// the end differs, and rank 0's output is the same full frame.  CTA b only
+// ever reads and writes slice b, so the ordering is per slice: CTA b
+// publishes "slice b reached stage s" with a system-scope release add on its
+// own counter, and reads a peer's slice b after an acquire load of that
+// peer's slice-b counter.  There is no grid-wide barrier inside a rank, so
+// nothing requires the grid to be co-resident: with CTAs dispatched in index
+// order the lowest unfinished slice always runs on every rank, which keeps a
+// swap that shares the GPU with other kernels (in situ: the simulation's)
+// progressing.  Spin-waits are bounded by a timeout that surfaces as
+// TransportError instead of a hung GPU.
 #include <cstring>
 
 #include "common.cuh"
 
 namespace isc {
 
-constexpr int kFlagWords = 16;
+// Flag block of one rank: kCtrlWords control words (kErrWord = transport
+// error), then per-slice arrival counters, word kCtrlWords + stage *
+// ISC_MAX_SWAP_CTAS + slice.  Stages: 0 image ready, r+1 round r done,
+// rounds+1 final span stored into rank 0's output, kRootReadStage rank 0 has
+// read the slice (direct send).  Every counter grows by exactly one per
+// epoch, so "stage reached in epoch e" is "counter >= e".
+constexpr int kCtrlWords = 16;
 constexpr int kErrWord = 9;
-constexpr int kRootReadWord = 8;
+constexpr int kStages = ISC_SWAP_STAGES;
+constexpr int kRootReadStage = kStages - 1;
+constexpr int kFlagWords = kCtrlWords + kStages * ISC_MAX_SWAP_CTAS;
+static_assert(ISC_MAX_ROUNDS + 2 <= kRootReadStage, "stage words overlap");
+
+__device__ __forceinline__ unsigned long long* stage_word(unsigned long long* flags, int stage, int slice) {
+  return flags + kCtrlWords + stage * ISC_MAX_SWAP_CTAS + slice;
+}
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
   unsigned long long v;
@@ -57,11 +83,12 @@ __device__ bool wait_at_least(const unsigned long long* p, unsigned long long ta
   return true;
 }
 
-__device__ __forceinline__ void publish(unsigned long long* flags, int word) {
+// Whole CTA: every thread's prior writes, then thread 0 bumps the counter.
+__device__ __forceinline__ void publish(unsigned long long* counter) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence_system();
-    red_release_sys(flags + word, 1ull);
+    red_release_sys(counter, 1ull);
   }
 }
 
@@ -129,80 +156,77 @@ __device__ __forceinline__ void copy_span(float4* out, const float4* in, long lo
   for (; i < c1; i += stride) out[i] = __ldcg(in + i);
 }
 
-__device__ __forceinline__ void cta_chunk(long long lo, long long hi, long long& a, long long& b) {
-  const long long n = hi - lo;
-  const long long per = (n + gridDim.x - 1) / gridDim.x;
-  a = lo + per * blockIdx.x;
-  b = min(hi, a + per);
-  if (a > hi) a = hi;
+// Slice b of n pixels cut into `parts` contiguous slices.
+__device__ __forceinline__ void slice_of(long long n, int parts, int b, long long& a, long long& e) {
+  const long long per = (n + parts - 1) / parts;
+  a = min(n, per * b);
+  e = min(n, a + per);
 }
 
 __global__ void __launch_bounds__(512) swap_kernel(const __grid_constant__ isc_swap_args a) {
   const int R = a.size;
+  const int b = blockIdx.x;
   int v = 0;
   for (int i = 0; i < R; ++i)
     if (a.order[i] == a.rank) v = i;
   int rounds = 0;
   while ((1 << rounds) < R) ++rounds;
   unsigned long long* me = a.flags[a.rank];
-  const unsigned long long target = (unsigned long long)a.epoch * (unsigned long long)a.n_ctas;
+  const unsigned long long target = (unsigned long long)a.epoch;
   float4* mine = reinterpret_cast<float4*>(a.image[a.rank]);
 
-  if (a.publish_ready) publish(me, 0);  // image ready (stream-ordered after render)
+  // slice b of the image is ready (stream-ordered after the render)
+  if (a.publish_ready) publish(stage_word(me, 0, b));
 
-  long long lo = 0, hi = a.n_pixels;
+  long long lo, hi;
+  slice_of(a.n_pixels, a.n_ctas, b, lo, hi);
   for (int r = 0; r < rounds; ++r) {
     const int bit = 1 << r;
     const int pv = v ^ bit;
-    const long long mid = (lo + hi) / 2;
+    const long long mid = (lo + hi) / 2;          // compositing.py:150
     const bool keep_high = (v & bit) != 0;
     const long long klo = keep_high ? mid : lo, khi = keep_high ? hi : mid;
     if (r >= a.round_begin && r < a.round_end) {
       const int partner = a.order[pv];
-      if (!cta_wait(a.flags[partner] + r, target, a.timeout_ns, me)) return;
-      if (r > 0 && !cta_wait(me + r, target, a.timeout_ns, me)) return;
-      const float4* theirs = reinterpret_cast<const float4*>(a.image[partner]);
-      long long c0, c1;
-      cta_chunk(klo, khi, c0, c1);
-      over_span(mine, theirs, c0, c1, pv < v);
-      publish(me, r + 1);
+      // the partner finished round r-1 on slice b (r = 0: its image is
+      // ready); this CTA's own round r-1 precedes it in program order (or,
+      // launched round by round, in stream order)
+      if (!cta_wait(stage_word(a.flags[partner], r, b), target, a.timeout_ns, me)) return;
+      over_span(mine, reinterpret_cast<const float4*>(a.image[partner]), klo, khi, pv < v);
+      publish(stage_word(me, r + 1, b));
     }
     lo = klo;
     hi = khi;
   }
 
   if (a.collect) {
-    if (!cta_wait(me + rounds, target, a.timeout_ns, me)) return;
-    float4* out = reinterpret_cast<float4*>(a.root_out);
-    long long c0, c1;
-    cta_chunk(lo, hi, c0, c1);
-    copy_span(out, mine, c0, c1);
-    publish(me, rounds + 1);
+    copy_span(reinterpret_cast<float4*>(a.root_out), mine, lo, hi);
+    publish(stage_word(me, rounds + 1, b));
   }
 
-  if (a.finish && blockIdx.x == 0) {
+  if (a.finish) {
     if (a.rank == 0) {
+      // every rank's final span of slice b has landed in the output
       for (int q = 0; q < R; ++q)
-        if (!cta_wait(a.flags[q] + rounds + 1, target, a.timeout_ns, me)) return;
+        if (!cta_wait(stage_word(a.flags[q], rounds + 1, b), target, a.timeout_ns, me)) return;
     } else {
-      int vv = v;
-      for (int r = 0; r < rounds; ++r) {
-        const int partner = a.order[vv ^ (1 << r)];
-        if (!cta_wait(a.flags[partner] + r + 1, target, a.timeout_ns, me)) return;
-      }
+      // every partner has finished reading this rank's slice b
+      for (int r = 0; r < rounds; ++r)
+        if (!cta_wait(stage_word(a.flags[a.order[v ^ (1 << r)]], r + 1, b), target, a.timeout_ns, me)) return;
     }
   }
 }
 
 __global__ void __launch_bounds__(512) direct_send_kernel(const __grid_constant__ isc_swap_args a) {
+  const int b = blockIdx.x;
   unsigned long long* me = a.flags[a.rank];
-  const unsigned long long target = (unsigned long long)a.epoch * (unsigned long long)a.n_ctas;
-  if (a.publish_ready) publish(me, 0);
+  const unsigned long long target = (unsigned long long)a.epoch;
+  if (a.publish_ready) publish(stage_word(me, 0, b));
+  long long c0, c1;
+  slice_of(a.n_pixels, a.n_ctas, b, c0, c1);
   if (a.rank == 0) {
     for (int q = 0; q < a.size; ++q)
-      if (!cta_wait(a.flags[q], target, a.timeout_ns, me)) return;
-    long long c0, c1;
-    cta_chunk(0, a.n_pixels, c0, c1);
+      if (!cta_wait(stage_word(a.flags[q], 0, b), target, a.timeout_ns, me)) return;
     float4* out = reinterpret_cast<float4*>(a.root_out);
     for (long long i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -210,9 +234,9 @@ __global__ void __launch_bounds__(512) direct_send_kernel(const __grid_constant_
         acc = over4(acc, __ldcg(reinterpret_cast<const float4*>(a.image[a.order[r]]) + i));
       out[i] = acc;
     }
-    publish(me, kRootReadWord);
-  } else if (a.finish && blockIdx.x == 0) {
-    cta_wait(a.flags[0] + kRootReadWord, target, a.timeout_ns, me);
+    publish(stage_word(me, kRootReadStage, b));
+  } else if (a.finish) {
+    cta_wait(stage_word(a.flags[0], kRootReadStage, b), target, a.timeout_ns, me);
   }
 }
 
@@ -230,7 +254,7 @@ static int check_swap(const isc_swap_args* a, bool pow2) {
   if (a->size < 1 || a->size > ISC_MAX_RANKS) return fail(ISC_E_COMPOSITE, "world size out of range");
   if (a->rank < 0 || a->rank >= a->size) return fail(ISC_E_COMPOSITE, "rank out of range");
   if (pow2 && (a->size & (a->size - 1))) return fail(ISC_E_COMPOSITE, "binary swap needs a power-of-two size");
-  if (a->n_ctas < 1 || a->n_ctas > 4096) return fail(ISC_E_COMPOSITE, "n_ctas out of range");
+  if (a->n_ctas < 1 || a->n_ctas > ISC_MAX_SWAP_CTAS) return fail(ISC_E_COMPOSITE, "n_ctas out of range");
   if (a->epoch < 1) return fail(ISC_E_COMPOSITE, "epoch must start at 1");
   unsigned seen = 0;
   unsigned long long seen_hi = 0;
@@ -305,6 +329,32 @@ extern "C" int isc_swap_status(unsigned long long* flags, void* stream, unsigned
     ISC_CUDA_CHECK(cudaMemsetAsync(flags + kErrWord, 0, sizeof(unsigned long long), s));
     ISC_CUDA_CHECK(cudaStreamSynchronize(s));
   }
+  return ISC_OK;
+}
+
+extern "C" int isc_swap_error_async(unsigned long long* flags, unsigned long long* pinned, void* stream) {
+  if (!flags || !pinned) return fail(ISC_E_VALUE, "null argument");
+  ISC_CUDA_CHECK(cudaMemcpyAsync(pinned, flags + kErrWord, sizeof(*pinned), cudaMemcpyDeviceToHost,
+                                 reinterpret_cast<cudaStream_t>(stream)));
+  return ISC_OK;
+}
+
+extern "C" int isc_swap_reset(unsigned long long* flags, void* stream) {
+  if (!flags) return fail(ISC_E_VALUE, "null flag block");
+  ISC_CUDA_CHECK(cudaMemsetAsync(flags, 0, sizeof(unsigned long long) * kFlagWords,
+                                 reinterpret_cast<cudaStream_t>(stream)));
+  return ISC_OK;
+}
+
+__global__ void occupy_kernel(long long ns) {
+  const unsigned long long t0 = global_ns();
+  while ((long long)(global_ns() - t0) < ns) __nanosleep(1000);
+}
+
+extern "C" int isc_debug_occupy(int32_t n_ctas, int32_t threads, int64_t ns, void* stream) {
+  if (n_ctas < 1 || threads < 1 || threads > 1024 || ns < 0) return fail(ISC_E_VALUE, "bad occupy arguments");
+  occupy_kernel<<<n_ctas, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(ns);
+  ISC_CUDA_CHECK(cudaGetLastError());
   return ISC_OK;
 }
 

@@ -69,11 +69,11 @@ class OccupancyTuner {
       Entry* e = find(k);
       return e ? (e->decided ? e->best : e->provisional) : kCand[0];
     }
-    // trials only for a key rendered twice in a row (a static view): a
-    // camera sweep (orbit) never pays for trials it cannot reuse
-    const bool repeat = have_last_ && last_ == k;
-    last_ = k;
-    have_last_ = true;
+    // trials only for a key rendered again within this thread's last kRecent
+    // renders (a static view, also when one thread renders several ranks'
+    // bricks in turn): a camera sweep such as the 26-view orbit never pays
+    // for trials it cannot reuse
+    const bool repeat = seen_recently(k);
     Entry* e = find(k);
     if (!e && !repeat) return kCand[0];
     if (!e) {
@@ -85,7 +85,15 @@ class OccupancyTuner {
     // finish the stage whose trials have all completed
     if (e->trials == e->planned && done(*e)) {
       float t[3] = {0.f, 0.f, 0.f};
-      for (int i = 0; i < e->planned; ++i) cudaEventElapsedTime(&t[i], e->ev[i][0], e->ev[i][1]);
+      for (int i = 0; i < e->planned; ++i) {
+        if (cudaEventElapsedTime(&t[i], e->ev[i][0], e->ev[i][1]) != cudaSuccess) {
+          cudaGetLastError();  // never leave a sticky error for the caller's next check
+          e->best = kCand[0];
+          e->decided = true;
+          release(*e);
+          return e->best;
+        }
+      }
       int best = 0;
       for (int i = 1; i < e->planned; ++i)
         if (t[i] < t[best]) best = i;
@@ -147,10 +155,22 @@ class OccupancyTuner {
     for (auto& e : entries_) release(e);
     entries_.clear();
   }
+  static constexpr int kRecent = 8;
+  static bool seen_recently(const Key& k) {
+    thread_local Key ring[kRecent];
+    thread_local int used = 0, next = 0;
+    bool hit = false;
+    for (int i = 0; i < used; ++i)
+      if (ring[i] == k) hit = true;
+    if (!hit) {
+      ring[next] = k;
+      next = (next + 1) % kRecent;
+      if (used < kRecent) ++used;
+    }
+    return hit;
+  }
   std::mutex mu_;
   std::deque<Entry> entries_;
-  Key last_{};
-  bool have_last_ = false;
 };
 
 static OccupancyTuner& tuner() {

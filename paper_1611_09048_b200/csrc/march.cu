@@ -150,11 +150,18 @@ __global__ void __launch_bounds__(kThreads) march_kernel(const __grid_constant__
           }
           // ---- iso: raycast.py:384-468 ----
           const float thr = s.iso_threshold;
-          const bool exact = s.has_guard && INTERP;
+          const bool guarded_interp = s.has_guard && INTERP;
+          const bool exact = guarded_interp && !a.no_layout;
           float before = prev[si];
           if (k == r.k_lo && k - 1 >= r.kg_lo) {  // entry pair through the guard
             double pq[3];
             station_pos(o, r.d, dmul((double)(k - 1), a.step), pq);
+            if (guarded_interp && a.no_layout) {
+              // no layout knowledge: clamp into reach (raycast.py:404-409)
+#pragma unroll
+              for (int i = 0; i < 3; ++i)
+                pq[i] = dmin(dmax(pq[i], b.offset[i] - b.guard), b.offset[i] + bsz[i] + b.guard - 1 - 1e-9);
+            }
             before = (!exact || reachable(b.offset, bsz, b.guard, pq)) ? scalar_at<false>(s, b, pq, INTERP, err)
                                                                      : CUDART_NAN_F;
           }
@@ -577,6 +584,16 @@ static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_
   static const int tw_env = getenv("ISC_TILE_W") ? __builtin_ctz(atoi(getenv("ISC_TILE_W"))) : -1;
   static const int cap_env = getenv("ISC_CTAS_PER_SM") ? atoi(getenv("ISC_CTAS_PER_SM")) : 0;
   static const bool no_tune = getenv("ISC_DISABLE_TUNE") != nullptr;
+  // screen-rectangle cull first: a brick entirely off screen launches
+  // nothing, and must not open tuner trials whose events are never recorded
+  int rx0, ry0, rx1, ry1;
+  static const bool no_cull = getenv("ISC_DISABLE_CULL") != nullptr;
+  const bool culled = !no_cull && brick_screen_rect(a, rx0, ry0, rx1, ry1);
+  if (culled) {
+    // pixels outside the rectangle miss the brick: transparent
+    ISC_CUDA_CHECK(cudaMemsetAsync(a->out_rgba, 0, (size_t)a->camera.width * a->camera.height * sizeof(float4), st));
+    if (rx1 <= rx0 || ry1 <= ry0) return ISC_OK;
+  }
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   OccupancyTuner::Choice ch{cap_env, tw_env >= 0 ? tw_env : 3};
   if (!cap_env && tw_env < 0 && !no_tune && PAIRED) {
@@ -588,16 +605,11 @@ static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_
   const int tw = 1 << tw_log2, th = (PAIRED ? 16 : 32) >> tw_log2;
   int tiles_x = (a->camera.width + tw - 1) / tw, tiles_y = (a->camera.height + th - 1) / th;
   int tile_x0 = 0, tile_y0 = 0;
-  int rx0, ry0, rx1, ry1;
-  static const bool no_cull = getenv("ISC_DISABLE_CULL") != nullptr;
-  if (!no_cull && brick_screen_rect(a, rx0, ry0, rx1, ry1)) {
-    // pixels outside the rectangle miss the brick: transparent
-    ISC_CUDA_CHECK(cudaMemsetAsync(a->out_rgba, 0, (size_t)a->camera.width * a->camera.height * sizeof(float4), st));
+  if (culled) {
     tile_x0 = rx0 / tw;
     tile_y0 = ry0 / th;
-    tiles_x = rx1 > rx0 ? (rx1 + tw - 1) / tw - tile_x0 : 0;
-    tiles_y = ry1 > ry0 ? (ry1 + th - 1) / th - tile_y0 : 0;
-    if (tiles_x == 0 || tiles_y == 0) return ISC_OK;
+    tiles_x = (rx1 + tw - 1) / tw - tile_x0;
+    tiles_y = (ry1 + th - 1) / th - tile_y0;
   }
   const int super_x = (tiles_x + 7) / 8, super_y = (tiles_y + 7) / 8;
   static const bool row_order = getenv("ISC_TILE_ROWS") != nullptr;
@@ -669,8 +681,10 @@ extern "C" int isc_render_local(const isc_render_args* a, void* stream) {
     return paired ? launch_fast<false, false, true>(a, F, s) : launch_fast<false, false, false>(a, F, s);
   }
   static const bool no_multi = getenv("ISC_DISABLE_MULTI") != nullptr;
+  bool layout_free_iso = false;  // march_rays(volume=None) with an iso source: generic kernel only
+  for (int i = 0; i < a->n_sources; ++i) layout_free_iso |= a->no_layout && a->src[i].mode == ISC_ISO;
   int mstatus = ISC_OK;
-  if (!no_multi && launch_multi(a, s, &mstatus)) return mstatus;
+  if (!no_multi && !layout_free_iso && launch_multi(a, s, &mstatus)) return mstatus;
   dim3 grid((a->camera.width + kTile - 1) / kTile, (a->camera.height + kTile - 1) / kTile);
   const size_t smem = (size_t)a->n_sources * ISC_LUT_ENTRIES * sizeof(float4);
   if (a->interpolation) march_kernel<true><<<grid, kThreads, smem, s>>>(*a);

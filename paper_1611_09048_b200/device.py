@@ -13,6 +13,7 @@ import torch
 from . import _abi
 
 _DTYPES = {torch.float32: _abi.F32, torch.float64: _abi.F64, torch.float16: _abi.F16, torch.bfloat16: _abi.BF16}
+DEVICE_DTYPES = frozenset(_DTYPES)   # dtypes the kernels read in place
 
 
 _CUDA_OK = False

@@ -28,7 +28,7 @@ import numpy as np
 import torch
 
 from . import _abi
-from .device import LUTS, as_device_field, dtype_code, ptr, require_cuda, stream_handle
+from .device import DEVICE_DTYPES, LUTS, as_device_field, dtype_code, ptr, require_cuda, stream_handle
 from .errors import FieldError, GuardContractError
 from .fields import LocalDomain, SourceHandle, SourceRegistry
 from .functors import ChainLimits, FunctorChain, FunctorRegistry, device_program, parse_chain
@@ -223,29 +223,35 @@ class _ArgsCache:
         self.capacity = capacity
 
     @staticmethod
-    def _fingerprint(plans, domain):
+    def _fingerprint(plans, domain, device):
         fp, fields = [], []
         for plan in plans:
             array, guard = plan.handle.device_view(domain)
-            if not (isinstance(array, torch.Tensor) and array.is_cuda):
+            # only zero-copy sources: a CUDA tensor on the render device whose
+            # dtype the kernels read directly.  Anything as_device_field would
+            # convert or move (integer dtypes, another GPU) gets a fresh copy
+            # per frame, and a block pointing at last frame's copy would read
+            # freed (and stale) memory.
+            if not (isinstance(array, torch.Tensor) and array.is_cuda and array.device == device
+                    and array.dtype in DEVICE_DTYPES):
                 return None, None
             fp.append((array.data_ptr(), tuple(array.shape), tuple(array.stride()), array.dtype, guard,
                        hash(np.ascontiguousarray(plan.tf.lut).tobytes())))
             fields.append(array)
         return tuple(fp), fields
 
-    def get(self, key, objects, plans, domain):
+    def get(self, key, objects, plans, domain, device):
         with self._lock:
             e = self._entries.get(key)
         if e is None or any(r() is not o for r, o in zip(e[3], objects)):
             return None
-        fp, fields = self._fingerprint(plans, domain)
+        fp, fields = self._fingerprint(plans, domain, device)
         if fp is None or fp != e[1]:
             return None
         return _abi.RenderArgs.from_buffer_copy(e[0]), list(e[2]) + fields
 
-    def put(self, key, objects, plans, domain, args, keep):
-        fp, _ = self._fingerprint(plans, domain)
+    def put(self, key, objects, plans, domain, device, args, keep):
+        fp, _ = self._fingerprint(plans, domain, device)
         if fp is None:
             return
         try:
@@ -343,13 +349,13 @@ def render_local(rank_ctx, scene: SceneState, plans: Optional[Sequence[SourcePla
     keep: list = []
     objects = (scene, *plans, domain, volume)
     key = (tuple(id(o) for o in objects), analytic_lut, device.index)
-    hit = _ARGS.get(key, objects, plans, domain)
+    hit = _ARGS.get(key, objects, plans, domain, device)
     if hit is not None:
         args, kept = hit
         keep.extend(kept)
     else:
         args = pack_render_args(domain, volume, scene, plans, device, keep, analytic_lut)
-        _ARGS.put(key, objects, plans, domain, args, keep)
+        _ARGS.put(key, objects, plans, domain, device, args, keep)
     if out is None:
         out = torch.empty((h, w, 4), dtype=torch.float32, device=device)
     elif out.shape != (h, w, 4) or out.dtype != torch.float32 or not out.is_contiguous() or out.device != device:
@@ -433,8 +439,9 @@ class _RayListScene:
 
 
 class _WholeVolume:
-    """march_rays(volume=None): the brick is the whole volume (no neighbour
-    owns an iso pair; entry pairs come from the global interval only)."""
+    """Layout stand-in when the caller gives no GlobalVolume: the brick is the
+    whole volume.  march_rays(volume=None) also sets ``no_layout`` so iso entry
+    pairs are clamped into the guard reach (raycast.py:404-409)."""
 
     def __init__(self, domain):
         self.size = tuple(int(domain.offset[a]) + int(domain.size[a]) for a in range(3))
@@ -468,6 +475,7 @@ def march_rays(origin, dirs, local_interval, global_interval, plans: Sequence[So
     kr = torch.empty((n, 4), dtype=torch.int32, device=device) if station_recorder is not None else None
     stats = torch.zeros(3, dtype=torch.int64, device=device)
     args.ray_dirs, args.ray_intervals = ptr(dirs_t), ptr(iv_t)
+    args.no_layout = 1 if volume is None else 0
     args.out_rgba = ptr(out)
     args.out_stations = ptr(counts) if counts is not None else None
     args.out_krange = ptr(kr) if kr is not None else None

@@ -104,18 +104,28 @@ def merge_metadata(per_rank_docs: Sequence[dict]) -> dict:
 class FrameStreamer:
     """Root-side background encode + send, one frame in flight (runtime.py:187-249).
 
-    ``submit`` quantises the frame on the device, starts its D2H on a side
-    stream and returns; a worker thread waits for the copy, encodes and calls
-    ``sink(message)``.  ``wait_previous`` is the single per-frame rendezvous.
+    ``submit`` quantises the frame on the device (``to_rgba8``), starts its
+    D2H on a side stream and returns; a worker thread waits for the copy,
+    encodes and calls ``sink(message)`` with the reference's message schema
+    (``type``, ``step``, ``image: {width, height, encoding, data}``,
+    ``metadata``, ``scene``: the scene echo, runtime.py:222-235).
+    ``wait_previous`` is the single per-frame rendezvous; submitting while a
+    frame is in flight raises, as in the reference.  ``encoder(data,
+    encoding, quality)`` receives the already-quantised uint8 (H, W, 4)
+    frame (the 8-bit quantisation runs on the GPU).
     """
 
-    def __init__(self, sink: Callable[[dict], None], encoding: str = RAW_RGBA8):
+    def __init__(self, sink: Callable[[dict], None],
+                 encoder: Optional[Callable[[np.ndarray, str, Optional[int]], str]] = None,
+                 encoding: str = RAW_RGBA8, quality: Optional[int] = None):
         import torch
         self.sink = sink
+        self.encoder = encoder or (lambda data, enc, _q: _encode_bytes(data, enc))
         self.encoding = encoding
+        self.quality = quality
         self.timeline: list = []
-        self._thread: Optional[threading.Thread] = None
-        self._error: Optional[BaseException] = None
+        self._pending: Optional[threading.Thread] = None
+        self._failure: Optional[BaseException] = None
         self._stream = torch.cuda.Stream()
         self._host = None
 
@@ -123,16 +133,17 @@ class FrameStreamer:
         self.timeline.append((event, step, time.monotonic()))
 
     def wait_previous(self) -> None:
-        if self._thread is not None:
-            self._thread.join()
-            self._thread = None
-        if self._error is not None:
-            err, self._error = self._error, None
-            raise RuntimeError(f"frame sink failed: {err}") from err
+        if self._pending is not None:
+            self._pending.join()
+            self._pending = None
+        if self._failure is not None:
+            failure, self._failure = self._failure, None
+            raise failure
 
     def submit(self, frame, step: int, metadata: dict, scene: SceneState) -> None:
         import torch
-        self.wait_previous()
+        if self._pending is not None:
+            raise RuntimeError("previous frame still in flight; wait_previous() first")
         q = to_rgba8(frame)
         ready = torch.cuda.Event()
         ready.record()
@@ -143,24 +154,31 @@ class FrameStreamer:
         with torch.cuda.stream(self._stream):
             host.copy_(q, non_blocking=True)
             q.record_stream(self._stream)
-        done = torch.cuda.Event()
-        done.record(self._stream)
+        copied = torch.cuda.Event()
+        copied.record(self._stream)
         h, w = int(q.shape[0]), int(q.shape[1])
+        scene_doc = scene.to_json()
 
-        def work():
+        def job():
             try:
                 self.mark("send_begin", step)
-                done.synchronize()
-                msg = {"type": "frame", "step": step, "width": w, "height": h, "encoding": self.encoding,
-                       "data": _encode_bytes(host.numpy(), self.encoding), "metadata": metadata,
-                       "scene_version": scene.version}
-                self.sink(msg)
-                self.mark("send_end", step)
+                copied.synchronize()
+                self.sink({"type": "frame", "step": step,
+                           "image": {"width": w, "height": h, "encoding": self.encoding,
+                                     "data": self.encoder(host.numpy(), self.encoding, self.quality)},
+                           "metadata": metadata, "scene": scene_doc})
             except BaseException as exc:  # noqa: BLE001 -- surfaced at the rendezvous
-                self._error = exc
+                self._failure = exc
+            finally:
+                self.mark("send_end", step)
 
-        self._thread = threading.Thread(target=work, daemon=True)
-        self._thread.start()
+        self._pending = threading.Thread(target=job, daemon=True)
+        self._pending.start()
+
+    def close(self) -> None:
+        if self._pending is not None:
+            self._pending.join()
+            self._pending = None
 
 
 @dataclass

@@ -16,9 +16,10 @@
 
 from __future__ import annotations
 
+import collections
 import ctypes as C
-import queue
 import threading
+import time
 from typing import Callable, Optional, Protocol
 
 from .errors import TransportError
@@ -39,13 +40,17 @@ class Transport(Protocol):
 
 
 class LocalFabric:
-    """FIFO queue per (src, dst) with byte counters (transport.py:31-71)."""
+    """In-process rank fabric with the reference's semantics
+    (transport.py:31-71): messages are delivered reliably and in order per
+    (sender, receiver) pair, a receive gives up after a timeout with
+    TransportError, and per-rank byte counters back the compositing balance
+    checks.  Built on one condition-variable mailbox per receiving rank."""
 
     def __init__(self, size: int, default_timeout: float = 120.0):
         self.size = size
         self.default_timeout = default_timeout
-        self._queues = {(s, d): queue.Queue() for s in range(size) for d in range(size)}
-        self._lock = threading.Lock()
+        self._mail = [_Mailbox(size) for _ in range(size)]
+        self._count_lock = threading.Lock()
         self.sent_bytes = [0] * size
         self.received_bytes = [0] * size
 
@@ -53,64 +58,82 @@ class LocalFabric:
         return LocalTransport(self, rank)
 
     def endpoints(self) -> list:
-        return [LocalTransport(self, r) for r in range(self.size)]
+        return list(map(self.endpoint, range(self.size)))
 
     def reset_counters(self) -> None:
-        with self._lock:
+        with self._count_lock:
             self.sent_bytes = [0] * self.size
             self.received_bytes = [0] * self.size
 
+    def _count(self, counters: list, rank: int, n: int) -> None:
+        with self._count_lock:
+            counters[rank] += n
+
     def _send(self, src: int, dst: int, data: bytes) -> None:
-        if not 0 <= dst < self.size:
+        if dst < 0 or dst >= self.size:
             raise TransportError(f"destination rank {dst} out of range")
-        with self._lock:
-            self.sent_bytes[src] += len(data)
-        self._queues[(src, dst)].put(data)
+        self._count(self.sent_bytes, src, len(data))
+        self._mail[dst].put(src, data)
 
     def _receive(self, src: int, dst: int, timeout: Optional[float]) -> bytes:
-        try:
-            data = self._queues[(src, dst)].get(timeout=self.default_timeout if timeout is None else timeout)
-        except queue.Empty:
-            raise TransportError(f"rank {dst} timed out waiting for rank {src}") from None
-        with self._lock:
-            self.received_bytes[dst] += len(data)
+        limit = self.default_timeout if timeout is None else timeout
+        data = self._mail[dst].take(src, limit)
+        if data is None:
+            raise TransportError(f"rank {dst} timed out waiting for rank {src}")
+        self._count(self.received_bytes, dst, len(data))
         return data
 
 
+class _Mailbox:
+    """Per-sender FIFOs of one receiving rank behind a single condition variable."""
+
+    def __init__(self, senders: int):
+        self._fifo = [collections.deque() for _ in range(senders)]
+        self._cv = threading.Condition()
+
+    def put(self, src: int, data: bytes) -> None:
+        with self._cv:
+            self._fifo[src].append(data)
+            self._cv.notify_all()
+
+    def take(self, src: int, timeout: float) -> Optional[bytes]:
+        with self._cv:
+            if not self._cv.wait_for(lambda: len(self._fifo[src]) > 0, timeout):
+                return None
+            return self._fifo[src].popleft()
+
+
 class _HostCollectives:
-    """broadcast / gather written once on top of send / receive (transport.py:86-103)."""
+    """broadcast / gather / all-gather written once on top of send / receive
+    (the reference's LocalTransport collectives, transport.py:86-103)."""
 
     def broadcast_from_root(self, data: Optional[bytes] = None) -> bytes:
-        if self.rank == 0:
-            if data is None:
-                raise TransportError("root must provide broadcast data")
-            for other in range(1, self.size):
-                self.send(other, data)
-            return data
-        return self.receive(0)
+        if self.rank != 0:
+            return self.receive(0)
+        if data is None:
+            raise TransportError("root must provide broadcast data")
+        for dst in range(1, self.size):
+            self.send(dst, data)
+        return data
 
     def gather_to_root(self, data: bytes) -> Optional[list]:
-        if self.rank != 0:
-            self.send(0, data)
-            return None
-        return [data] + [self.receive(r) for r in range(1, self.size)]
+        if self.rank == 0:
+            return [data, *(self.receive(src) for src in range(1, self.size))]
+        self.send(0, data)
+        return None
 
     def all_gather(self, data: bytes) -> list:
-        docs = self.gather_to_root(data)
-        if self.rank == 0:
-            import pickle
-            blob = pickle.dumps(docs)
-            self.broadcast_from_root(blob)
-            return docs
         import pickle
-        return pickle.loads(self.broadcast_from_root(None))
+        docs = self.gather_to_root(data)
+        blob = self.broadcast_from_root(pickle.dumps(docs) if self.rank == 0 else None)
+        return docs if self.rank == 0 else pickle.loads(blob)
 
 
 class LocalTransport(_HostCollectives):
+    """One rank's endpoint on a LocalFabric."""
+
     def __init__(self, fabric: LocalFabric, rank: int):
-        self.fabric = fabric
-        self.rank = rank
-        self.size = fabric.size
+        self.fabric, self.rank, self.size = fabric, rank, fabric.size
 
     def send(self, to: int, data: bytes) -> None:
         self.fabric._send(self.rank, to, data)
@@ -120,28 +143,31 @@ class LocalTransport(_HostCollectives):
 
 
 def run_ranks(size: int, body: Callable, timeout: float = 300.0) -> list:
-    """One thread per rank over a LocalFabric; first failure re-raised (transport.py:106-133)."""
+    """``body(endpoint)`` on one daemon thread per rank over a fresh
+    LocalFabric; per-rank results in rank order.  A rank that is still running
+    after ``timeout`` raises TransportError; otherwise the lowest failing
+    rank's exception is re-raised (transport.py:106-133)."""
     fabric = LocalFabric(size)
-    results: list = [None] * size
-    errors: list = []
+    outcome: list = [None] * size          # ("ok", value) | ("err", exc)
 
-    def runner(r: int):
+    def runner(rank: int) -> None:
         try:
-            results[r] = body(fabric.endpoint(r))
-        except BaseException as exc:  # noqa: BLE001
-            errors.append((r, exc))
+            outcome[rank] = ("ok", body(fabric.endpoint(rank)))
+        except BaseException as exc:  # noqa: BLE001 -- surfaced below
+            outcome[rank] = ("err", exc)
 
     threads = [threading.Thread(target=runner, args=(r,), daemon=True) for r in range(size)]
     for t in threads:
         t.start()
+    deadline = time.monotonic() + timeout
     for t in threads:
-        t.join(timeout)
+        t.join(max(0.0, deadline - time.monotonic()))
         if t.is_alive():
             raise TransportError("rank thread did not finish (deadlock?)")
-    if errors:
-        r, exc = errors[0]
-        raise RuntimeError(f"rank {r} failed: {exc}") from exc
-    return results
+    for rank, (kind, val) in enumerate(outcome):
+        if kind == "err":
+            raise RuntimeError(f"rank {rank} failed: {val}") from val
+    return [val for _, val in outcome]
 
 
 class TorchDistTransport(_HostCollectives):
@@ -283,14 +309,20 @@ class NvlinkTransport(_HostCollectives):
             self.flags = [a.flags_ptr for a in group.arenas]
             self.root_out = group.arenas[0].out_ptr
             self._opened = []
+            self._agreed_ctas = group.n_ctas
         else:
             self.rank, self.size = host.rank, host.size
             dev = torch.cuda.current_device()
             self.arena = _Arena(n_pixels, dev)
             buf = (C.c_char * _abi.IPC_HANDLE_BYTES)()
             _abi.check(_abi.lib().isc_ipc_handle(C.c_void_p(self.arena.base), buf), "ipc handle")
-            mine = bytes(buf)
-            handles = host.all_gather(mine)
+            sms = _abi.lib().isc_device_sm_count(dev)
+            want = min(_abi.MAX_SWAP_CTAS, sms if sms > 0 else 148)
+            # every rank must slice the image identically: agree on the
+            # smallest grid any rank proposes (ranks may sit on different SKUs)
+            docs = host.all_gather(want.to_bytes(4, "little") + bytes(buf))
+            self._agreed_ctas = min(int.from_bytes(d[:4], "little") for d in docs)
+            handles = [d[4:] for d in docs]
             self._opened = []
             self.images, self.flags = [], []
             root_base = None
@@ -314,8 +346,10 @@ class NvlinkTransport(_HostCollectives):
         self._err_slots = [torch.zeros(1, dtype=torch.int64).pin_memory() for _ in range(4)]
         self._pending: list = []      # (event, slot) of deferred error checks
         self._next_slot = 0
-        sms = _abi.lib().isc_device_sm_count(self.arena.device_index)
-        self.n_ctas = max(1, sms if sms > 0 else 148)
+        # slices (= CTAs) of the swap kernel; equal on every rank by
+        # construction.  Changing it is a collective decision: set the same
+        # value on every rank.
+        self.n_ctas = self._agreed_ctas
         self.sent_bytes = 0
         self.received_bytes = 0
 
@@ -367,20 +401,26 @@ class NvlinkTransport(_HostCollectives):
 
     def check_errors(self, stream_ptr: int) -> None:
         """After a swap launch: synchronous check (``sync_errors``) or a
-        deferred one -- the error word is copied into a pinned slot on the
-        stream and examined once that copy has completed."""
+        deferred one -- the library copies the error word into a pinned slot
+        on the swap's own stream (``isc_swap_error_async``, the same raw
+        handle the kernel was launched on) and a torch event recorded on the
+        current stream after it tells when the slot can be read."""
         if self.sync_errors:
             self.status(stream_ptr)
             return
         import torch
+        cur = torch.cuda.current_stream()
+        if int(cur.cuda_stream) != int(stream_ptr):
+            raise TransportError("check_errors must run on the stream the swap was launched on")
         self._poll(block=len(self._pending) >= len(self._err_slots))
         slot = self._err_slots[self._next_slot]
         self._next_slot = (self._next_slot + 1) % len(self._err_slots)
-        stream = torch.cuda.ExternalStream(stream_ptr)
-        with torch.cuda.stream(stream):
-            slot.copy_(self._error_word(), non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(stream)
+        slot.zero_()
+        self._abi.check(self._abi.lib().isc_swap_error_async(C.c_void_p(self.flags[self.rank]),
+                                                             C.c_void_p(slot.data_ptr()), C.c_void_p(stream_ptr)),
+                        "swap error copy")
+        ev = torch.cuda.Event()
+        ev.record(cur)
         self._pending.append((ev, slot))
 
     def flush(self) -> None:
@@ -391,7 +431,25 @@ class NvlinkTransport(_HostCollectives):
         import torch
         flags = torch.as_tensor(_CudaArray(self.flags[self.rank], (16,), "<i8"),
                                 device=f"cuda:{self.arena.device_index}")
-        return flags[9:10]
+        return flags[self._abi.ERR_WORD:self._abi.ERR_WORD + 1]
+
+    def reset(self) -> None:
+        """Collective recovery after a TransportError: every rank drains its
+        stream, zeroes its own flag block and restarts at epoch 1 behind two
+        host barriers, so no rank polls a half-reset block.  (A timed-out
+        CTA leaves its counters one short for good, so without a reset
+        every later swap would time out too.)"""
+        import torch
+        from .device import stream_handle
+        torch.cuda.synchronize(self.arena.device_index)
+        self.host.all_gather(b"")
+        s = stream_handle()
+        self._abi.check(self._abi.lib().isc_swap_reset(C.c_void_p(self.flags[self.rank]), C.c_void_p(s)),
+                        "swap reset")
+        torch.cuda.synchronize(self.arena.device_index)
+        self.host.all_gather(b"")
+        self.epoch = 0
+        self._pending = []
 
     def _poll(self, block: bool, all_: bool = False) -> None:
         bad = False
@@ -431,9 +489,33 @@ class LocalNvlinkGroup:
                 for p in set(devices) - {d}:
                     _abi.check(_abi.lib().isc_enable_peer_access(p), "peer access")
         self.arenas = [_Arena(n_pixels, d) for d in devices]
+        sms = min(_abi.lib().isc_device_sm_count(d) for d in set(devices))
+        self.n_ctas = min(_abi.MAX_SWAP_CTAS, sms if sms > 0 else 148)
         self.fabric = LocalFabric(size)
         self.endpoints = [NvlinkTransport(self.fabric.endpoint(r), _local=(self, r)) for r in range(size)]
+
+    def set_n_ctas(self, n: int) -> None:
+        """Slice count of every rank's swap (must be equal across ranks)."""
+        for ep in self.endpoints:
+            ep.n_ctas = n
+
+    def reset(self) -> None:
+        """Zero every rank's flag block and restart all ranks at epoch 1."""
+        import torch
+        from .device import stream_handle
+        torch.cuda.synchronize()
+        for ep in self.endpoints:
+            with torch.cuda.device(ep.arena.device_index):
+                _abi_check_reset(ep.flags[ep.rank], stream_handle())
+            ep.epoch = 0
+            ep._pending = []
+        torch.cuda.synchronize()
 
     def close(self):
         for a in self.arenas:
             a.free()
+
+
+def _abi_check_reset(flags_ptr: int, stream: int) -> None:
+    from . import _abi
+    _abi.check(_abi.lib().isc_swap_reset(C.c_void_p(flags_ptr), C.c_void_p(stream)), "swap reset")

@@ -100,3 +100,20 @@ def test_gloo_transport_and_swap_schedule(tmp_path, world):
         image_bytes = images[0][..., 0].size * 16
         for r in range(world):   # balance bound (test_compositing.py:193-214), control bytes excluded
             assert res[r]["sent"] <= 2 * image_bytes + 256
+
+
+def test_bench_gpus_flag_launches_that_many_ranks():
+    """``python bench.py --gpus N`` outside torchrun starts N ranks itself (the
+    driver's scaling run must not silently measure one rank)."""
+    import json
+    import subprocess
+    import sys
+    bench = os.path.join(ROOT, "bench.py")
+    for n, decomp in ((2, [2, 1, 1]), (4, [2, 2, 1])):
+        out = subprocess.run([sys.executable, bench, "--gpus", str(n), "--dry-run"], capture_output=True,
+                             text=True, timeout=300)
+        assert out.returncode == 0, out.stderr[-2000:]
+        line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+        assert line["n_gpus"] == n and line["ranks_seen"] == n
+        assert line["rank_sum"] == n * (n - 1) // 2
+        assert line["decomposition"] == decomp

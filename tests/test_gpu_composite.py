@@ -68,6 +68,132 @@ def test_peer_memory_swap_concurrent_ranks(ranks):
     assert res["others_none"]
 
 
+def _over_np(front, back):
+    return front + (np.float32(1.0) - front[:, 3:4]) * back
+
+
+@pytest.mark.parametrize("order", [[0, 1], [1, 0]])
+def test_swap_needs_no_coresident_grid(order):
+    """The swap kernel must make progress with any subset of its CTAs
+    resident (in situ the simulation's kernels share the GPU, and CTAs are
+    only guaranteed to run eventually, not together).  Rank 0 runs the real
+    kernel with the maximum slice count (1024 CTAs of 512 threads: far more
+    than the 4 x 148 that fit on a B200 at once), while rank 1 is played by
+    a host thread that serves slices in index order -- the partner is
+    independent of this GPU's SM residency, as on a multi-GPU box.  Arenas
+    live in pinned host memory (device-accessible under unified
+    addressing).  A design with a grid-wide barrier deadlocks here; the
+    per-slice protocol completes and matches the composite."""
+    import ctypes as C
+    import threading
+    import time
+    import torch
+    from paper_1611_09048_b200 import _abi
+    lib = _abi.lib()
+    n, parts = 48 * 1024 + 77, _abi.MAX_SWAP_CTAS
+    words = lib.isc_flag_words()
+    ctrl = 16
+    rng = np.random.default_rng(5)
+    host = []
+    for _ in range(2):
+        a = rng.uniform(0, 1, (n, 1)).astype(np.float32)
+        host.append(np.concatenate([rng.uniform(0, 1, (n, 3)).astype(np.float32) * a, a], axis=1))
+    img = [torch.from_numpy(h.copy()).pin_memory() for h in host]
+    flags = [torch.zeros(words, dtype=torch.int64).pin_memory() for _ in range(2)]
+    root = torch.zeros((n, 4), dtype=torch.float32).pin_memory()
+    args = _abi.SwapArgs()
+    args.rank, args.size, args.n_ctas = 0, 2, parts
+    args.round_begin, args.round_end, args.collect, args.finish, args.publish_ready = 0, 64, 1, 1, 1
+    args.n_pixels, args.epoch, args.timeout_ns = n, 1, int(20e9)
+    for i in range(2):
+        args.order[i] = order[i]
+        args.image[i] = img[i].data_ptr()
+        args.flags[i] = flags[i].data_ptr()
+    args.root_out = root.data_ptr()
+    va, vb = order.index(0), order.index(1)
+    fa, fb = flags[0].numpy(), flags[1].numpy()
+    a_img, b_img, out = img[0].numpy(), img[1].numpy(), root.numpy()
+    failure = []
+
+    def word(stage, sl):
+        return ctrl + stage * parts + sl
+
+    def wait(arr, idx, deadline):
+        while arr[idx] < 1:
+            if time.monotonic() > deadline:
+                raise TimeoutError(f"flag {idx} never set")
+
+    def partner():          # rank 1: compositing.py:145-181 on each slice, in slice order
+        try:
+            deadline = time.monotonic() + 60.0
+            per = (n + parts - 1) // parts
+            fb[word(0, 0):word(0, parts)] = 1                # image ready
+            for sl in range(parts):
+                lo, hi = min(n, per * sl), min(n, per * sl + per)
+                mid = (lo + hi) // 2
+                k0, k1 = (mid, hi) if vb & 1 else (lo, mid)
+                wait(fa, word(0, sl), deadline)
+                mine, theirs = b_img[k0:k1], a_img[k0:k1]
+                b_img[k0:k1] = _over_np(theirs, mine) if va < vb else _over_np(mine, theirs)
+                fb[word(1, sl)] = 1
+                out[k0:k1] = b_img[k0:k1]
+                fb[word(2, sl)] = 1
+            for sl in range(parts):                          # rank 0 has read our half
+                wait(fa, word(1, sl), deadline)
+        except BaseException as exc:  # noqa: BLE001
+            failure.append(exc)
+
+    stream = torch.cuda.Stream()
+    t = threading.Thread(target=partner, daemon=True)
+    t.start()
+    _abi.check(lib.isc_binary_swap(C.byref(args), C.c_void_p(stream.cuda_stream)), "binary_swap")
+    stream.synchronize()
+    t.join(90)
+    assert not failure, failure
+    assert int(fa[_abi.ERR_WORD]) == 0, "rank 0 timed out waiting"
+    front, back = (host[0], host[1]) if order == [0, 1] else (host[1], host[0])
+    assert np.abs(out - _over_np(front, back)).max() <= TOL
+
+
+def test_swap_recovers_after_timeout_with_reset():
+    """A timed-out swap leaves counters short; reset() restores the group."""
+    import torch
+    import paper_1611_09048_b200 as P
+    from paper_1611_09048_b200.compositing import binary_swap_local
+    gold = load("composite_swap4.npz")
+    imgs = _images(gold)
+    order = [int(v) for v in gold["order"]]
+    h, w = imgs[0].shape[:2]
+    grp = P.LocalNvlinkGroup(len(imgs), h * w)
+    try:
+        grp.set_n_ctas(4)
+        ep = grp.endpoints[0]
+        ep.timeout_s = 0.2
+        with pytest.raises(P.TransportError):
+            P.binary_swap(ep, imgs[0], order)            # the other ranks never arrive
+        grp.reset()
+        for _ in range(2):
+            out = binary_swap_local(grp, imgs, order).cpu().numpy()
+            assert np.abs(out - gold["result"]).max() <= TOL
+    finally:
+        grp.close()
+
+
+def test_slice_count_must_agree():
+    import paper_1611_09048_b200 as P
+    from paper_1611_09048_b200.compositing import binary_swap_local
+    gold = load("composite_swap2.npz")
+    imgs = _images(gold)
+    h, w = imgs[0].shape[:2]
+    grp = P.LocalNvlinkGroup(2, h * w)
+    try:
+        grp.endpoints[1].n_ctas = 7
+        with pytest.raises(P.CompositeError):
+            binary_swap_local(grp, imgs, [0, 1])
+    finally:
+        grp.close()
+
+
 @pytest.mark.parametrize("name", ["swap2", "swap8", "direct3", "direct6"])
 def test_byte_transport_swap_gpu_over(name):
     import paper_1611_09048_b200 as P
@@ -151,8 +277,17 @@ def test_swap_timeout_deferred_check():
         ep.n_ctas = 1
         ep.sync_errors = False
         P.binary_swap(ep, torch.zeros((8, 8, 4), device="cuda"), [0, 1])   # rank 1 never arrives
-        with pytest.raises(P.TransportError):
-            ep.flush()
+        torch.cuda.synchronize()
+        diag = (int(ep._error_word().item()), [int(s.item()) for s in ep._err_slots], len(ep._pending),
+                [int(v) for v in torch.as_tensor(P.transport._CudaArray(ep.flags[1], (32,), "<i8"), device="cuda")
+                 .cpu().tolist()])
+        with pytest.raises(P.TransportError, match="did not arrive"):
+            try:
+                ep.flush()
+            except P.TransportError:
+                raise
+            else:
+                raise AssertionError(f"no TransportError: {diag}")
         ep.flush()   # the error word was cleared: nothing pending
     finally:
         grp.close()

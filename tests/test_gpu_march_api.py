@@ -148,3 +148,37 @@ def test_march_rays_matches_oracle(mode):
     ref = O.render_rays(tuple(origin), dirs, O.Brick((0, 0, 0), (n, n, n), 1, (n, n, n)), [src])
     assert np.abs(got - ref.rgba).max() <= 1e-3
     assert stations == int(ref.stations.sum())
+
+
+@pytest.mark.parametrize("thr", [3.0, 5.0, 6.5])
+def test_march_rays_without_layout_clamps_iso_entry_pairs(thr):
+    """march_rays(volume=None) with a guarded trilinear iso source: the
+    reference clamps each entry pair's earlier station into the guard reach
+    instead of testing reachability, and checks no exit pairs
+    (raycast.py:396-418).  Golden from the real reference
+    (tests/golden/make_golden_march.py), rays entering a brick through its
+    upper y face; rays whose hit shading reads past the halo raise
+    GuardContractError there and here."""
+    import paper_1611_09048_b200 as P
+    from golden_io import load
+    torch = pytest.importorskip("torch")
+    gold = load("march_nolayout.npz")
+    off, size, g = tuple(int(v) for v in gold["offset"]), tuple(int(v) for v in gold["size"]), int(gold["guard"])
+    dom = P.LocalDomain(off, size, g)
+    handle = P.array_backed_handle(P.SourceDescriptor("d", 1, has_guard=True),
+                                   torch.from_numpy(gold["field"]).cuda(), g)
+    plan = P.SourcePlan(source_id=0, handle=handle, domain=dom, chain=P.identity_chain(1),
+                        tf=P.TransferFunction(gold["tf_lut"], (0.0, 12.0)), mode="iso", iso_threshold=thr)
+    settings = P.RenderSettings(active_set=(0,), modes={0: "iso"}, iso_thresholds={0: thr}, interpolation=True,
+                                step_length=0.5, early_termination_alpha=1.0)
+    raised = gold[f"raised_{thr}"]
+    ok = ~raised
+    rgba, stations = P.march_rays(gold["origin"], gold["dirs"][ok], (gold["t0"][ok], gold["t1"][ok]),
+                                  (gold["g0"][ok], gold["g1"][ok]), [plan], settings)
+    assert np.abs(rgba - gold[f"rgba_{thr}"][ok]).max() <= 1e-3
+    assert stations == int(gold[f"stations_{thr}"][ok].sum())
+    for i in np.nonzero(raised)[0]:
+        sl = slice(i, i + 1)
+        with pytest.raises(P.GuardContractError):
+            P.march_rays(gold["origin"], gold["dirs"][sl], (gold["t0"][sl], gold["t1"][sl]),
+                         (gold["g0"][sl], gold["g1"][sl]), [plan], settings)

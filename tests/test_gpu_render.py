@@ -601,3 +601,42 @@ def test_launch_block_cache_revalidates():
     P.update_sources(reg2, {0}, {})
     fresh = P.render_local(P.RankContext(vol, dom, reg2, fr, fr.limits), scene).pixels.cpu().numpy()
     assert np.array_equal(swapped, fresh) and not np.array_equal(swapped, first)
+
+
+def test_launch_block_not_cached_for_converted_fields():
+    """An integer field is converted to a float32 copy per frame (as the
+    reference casts every batch, fields.py:177); the launch block must not be
+    reused across frames (it would point at the previous frame's freed copy),
+    and an in-place update of the simulation's int array must show up."""
+    import paper_1611_09048_b200 as P
+    torch = _torch()
+    n = 16
+    rng = np.random.default_rng(37)
+    ai = torch.from_numpy(rng.integers(0, 4, (n + 2,) * 3).astype(np.int32)).cuda()
+    vol = P.GlobalVolume((n, n, n))
+    dom = vol.local_domain(0, 1)
+    reg = P.SourceRegistry(dom)
+    reg.register_handle(P.array_backed_handle(P.SourceDescriptor("f", 1, has_guard=True), ai, 1))
+    P.update_sources(reg, {0}, {})
+    fr = P.default_registry()
+    ctx = P.RankContext(vol, dom, reg, fr, fr.limits)
+    scene = _single_source_scene(P, n, (40.0, 30.0, -20.0), (8.0, 8.0, 8.0))
+    scene = P.SceneState(camera=scene.camera, tf_points=scene.tf_points, value_ranges={0: (0.0, 4.0)},
+                         chain_texts=scene.chain_texts, settings=scene.settings)
+    plans = P.build_plans(reg, fr, fr.limits, scene)
+
+    def frame():
+        img = P.render_local(ctx, scene, plans=plans).pixels.cpu().numpy()
+        junk = [torch.full((n + 2,) * 3, 1e6, device="cuda") for _ in range(4)]   # reuse freed blocks
+        del junk
+        return img
+
+    first = frame()
+    assert np.array_equal(frame(), first)
+    ai.add_(1)                                     # simulation updates its field in place
+    after = frame()
+    reg2 = P.SourceRegistry(dom)
+    reg2.register_handle(P.array_backed_handle(P.SourceDescriptor("g", 1, has_guard=True), ai.float(), 1))
+    P.update_sources(reg2, {0}, {})
+    want = P.render_local(P.RankContext(vol, dom, reg2, fr, fr.limits), scene).pixels.cpu().numpy()
+    assert np.array_equal(after, want) and not np.array_equal(after, first)

@@ -59,7 +59,14 @@ def test_frame_pipeline_single_rank_with_streamer():
     frame = results[-1].image
     assert np.abs(frame.cpu().numpy() - gold["d111_composite"]).max() <= 1e-3
     w, h = c["camera"]["image_size"]
-    assert np.array_equal(decode_frame(sent[-1]["data"], w, h), to_rgba8(frame).cpu().numpy())
+    msg = sent[-1]
+    # the reference's frame message schema (runtime.py:222-235, harness FrameSink
+    # reads message["image"][...], frontend FrameMessage protocol.ts:50-56)
+    assert set(msg) == {"type", "step", "image", "metadata", "scene"} and msg["type"] == "frame"
+    assert set(msg["image"]) == {"width", "height", "encoding", "data"}
+    assert (msg["image"]["width"], msg["image"]["height"]) == (w, h) and msg["image"]["encoding"] == "raw-rgba8"
+    assert P.SceneState.from_json(msg["scene"]).to_json() == ctx.scene.to_json()
+    assert np.array_equal(decode_frame(msg["image"]["data"], w, h), to_rgba8(frame).cpu().numpy())
     ev = [e for e, _, _ in streamer.timeline]
     assert ev.count("send_end") == 3 and results[-1].stations > 0 and results[-1].render_seconds > 0
 
