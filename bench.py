@@ -397,29 +397,41 @@ def run_b200(args):
     # to pinned host memory (D2H) every step.
     e2e = run_e2e(P, torch, dist, ctx, scenes[0], transport, canvas, order, rank, world, red_dev, max(2, k // 2))
 
-    # the same frame with the general shared-memory LUT lookup (no single-ramp
-    # shortcut), timed in this run for transparency
-    lut_path = None
-    if ctx_lut_applicable(P, scenes[0]):
+    # transfer-function variants of the same frame, timed in this run: the
+    # general shared-memory LUT lookup (no analytic form), and a 3-point
+    # transfer function (one slope change: the analytic hinge form, and the
+    # same through the LUT) -- what a user steering the TF gets
+    def time_tf(scene_v, analytic):
+        plans_v = P.build_plans(reg, fr, fr.limits, scene_v)
         evs2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
         for _ in range(2):
-            P.render_local(ctx, scenes[0], plans=plans[0], out=canvas, check_errors=False, analytic_lut=False)
+            P.render_local(ctx, scene_v, plans=plans_v, out=canvas, check_errors=False, analytic_lut=analytic)
         barrier()
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record(stream)
         for i in range(k):
-            P.render_local(ctx, scenes[i % len(scenes)], plans=plans[i % len(scenes)], out=canvas,
-                           check_errors=False, events=evs2[i], analytic_lut=False)
-            P.binary_swap(transport, canvas, orders[i % len(scenes)])
+            P.render_local(ctx, scene_v, plans=plans_v, out=canvas, check_errors=False, events=evs2[i],
+                           analytic_lut=analytic)
+            P.binary_swap(transport, canvas, order)
         s1.record(stream)
         torch.cuda.synchronize()
         kl = sum(x.elapsed_time(y) for x, y in evs2) / k
         tl = torch.tensor([s0.elapsed_time(s1) / k, kl], dtype=torch.float64, device=red_dev)
         if world > 1:
             dist.all_reduce(tl, op=dist.ReduceOp.MAX)
-        lut_path = {"value": round(1000.0 / float(tl[0]), 3), "unit": "frames/s", "kernel_ms": round(float(tl[1]), 4),
-                    "roofline_frac": round(float(br.item()) / (float(tl[1]) * 1e-3) / 1e9 / world / peak, 4),
-                    "note": "same frame, transfer function classified through the 256-entry shared-memory LUT"}
+        return {"value": round(1000.0 / float(tl[0]), 3), "unit": "frames/s", "kernel_ms": round(float(tl[1]), 4),
+                "roofline_frac": round(float(br.item()) / (float(tl[1]) * 1e-3) / 1e9 / world / peak, 4),
+                "kernel": describe_kernel(plans_v, scene_v.settings, analytic)}
+
+    lut_path = tf_variants = None
+    if len(scenes) == 1 and len(active) == 1:
+        lut_path = time_tf(scenes[0], False)
+        lut_path["note"] = "same frame, transfer function classified through the 256-entry shared-memory LUT"
+        tf3 = tf3_scene(P, scenes[0])
+        tf_variants = {"points": [list(p) for p in TF3_POINTS],
+                       "analytic": time_tf(tf3, True), "lut": time_tf(tf3, False),
+                       "note": "same frame with a 3-point transfer function (slope change at t=0.6): analytic "
+                               "hinge form (raycast.lut_analytic) vs the shared-memory LUT"}
 
     # informational: the same static-view frame replayed as one CUDA graph
     # (FrameGraph: no per-frame host preparation), N=1 only
@@ -465,10 +477,12 @@ def run_b200(args):
                          "kernel": describe_kernel(plans[0], scenes[0].settings), "kernel_ms": round(kernel_ms_max, 4),
                          "algorithmic_bytes_per_launch": int(br.item() / world)},
             "e2e": e2e,
-            "classification": ("analytic single-ramp transfer function (exact: the LUT is one straight run, "
-                               "so its lerp is base + slope*x); general shared-memory LUT path timed in "
-                               "'lut_path'") if lut_path else "shared-memory LUT",
+            "classification": ("analytic transfer function (exact: the LUT lerp is piecewise linear with "
+                               "few slope changes, raycast.lut_analytic); general shared-memory LUT path "
+                               "timed in 'lut_path', a 3-point TF in 'tf_3point'") if lut_path else
+                              "per-source analytic form or shared-memory LUT",
             "lut_path": lut_path,
+            "tf_3point": tf_variants,
             "graph_replay": graph_replay,
             "composite": composite,
             "e2e_host_field": host_field,
@@ -524,10 +538,13 @@ def run_e2e_host_field(P, torch, dist, ctx, scene, transport, canvas, order, ran
             "note": "field re-uploaded from pinned host memory every frame (not the in-situ case)"}
 
 
-def ctx_lut_applicable(P, scene):
-    from paper_1611_09048_b200.raycast import lut_line
-    sids = scene.settings.active_set
-    return len(sids) == 1 and lut_line(scene.transfer_function(sids[0]).lut) is not None
+TF3_POINTS = [(0.0, 0.0, 0.0, 0.0, 0.0), (0.6, 0.1, 0.7, 0.4, 0.3), (1.0, 0.7, 1.0, 0.9, 0.8)]
+
+
+def tf3_scene(P, scene):
+    """The scene with C3's 3-point 'cool' transfer function on source 0."""
+    return P.SceneState(camera=scene.camera, tf_points={0: TF3_POINTS}, value_ranges=scene.value_ranges,
+                        chain_texts=scene.chain_texts, settings=scene.settings, clip_planes=scene.clip_planes)
 
 
 def time_normalisation(P, torch, reg, domain, peak, reps=10):

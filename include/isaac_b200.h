@@ -57,11 +57,12 @@ extern "C" {
 
 #define ISC_ABI_VERSION 3  /* 2: isc_render_args.ray_dirs / ray_intervals, isc_gradient_normals;
                               3: per-slice swap counters, isc_swap_reset, isc_debug_occupy,
-                                 isc_render_args.no_layout */
+                                 isc_render_args.no_layout, piecewise-linear LUTs (lut_kinks) */
 #define ISC_MAX_SOURCES 8      /* active sources per render                 */
 #define ISC_MAX_CLIP_PLANES 8
 #define ISC_MAX_CHAIN 8        /* ChainLimits.max_length default is 5        */
 #define ISC_LUT_ENTRIES 256    /* scene.py:18                                 */
+#define ISC_MAX_LUT_KINKS 3    /* slope changes of an analytic LUT            */
 #define ISC_MAX_RANKS 64
 #define ISC_MAX_ROUNDS 6       /* log2(ISC_MAX_RANKS)                         */
 #define ISC_IPC_HANDLE_BYTES 64
@@ -113,13 +114,19 @@ typedef struct {
   int32_t n_steps;           /* chain length (0 = identity)               */
   const float* lut;          /* device, 256 x 4 straight RGBA (float32)  */
   isc_chain_step steps[ISC_MAX_CHAIN];
-  /* Optional analytic form of the LUT: when the 256 entries lie on one
-   * straight run (e.g. a two-point ramp), lut_linear = 1 and
-   * lut(x) = lut_base + lut_slope * x for x = 255 t exactly as the LUT lerp
-   * would give it; the kernel then skips the shared-memory lookup. */
+  /* Optional analytic form of the LUT.  The LUT lerp is the piecewise-linear
+   * interpolant through (i, lut[i]); when its slope changes at no more than
+   * ISC_MAX_LUT_KINKS integer positions (a tf_from_points ramp with a few
+   * control points, scene.py:113-126), lut_linear = 1 and
+   *   lut(x) = lut_base + lut_slope * x + sum_k lut_kink_dslope[k] * max(x - lut_kink_x[k], 0)
+   * for x = 255 t, exactly the LUT lerp; the kernel then skips the
+   * shared-memory lookup.  lut_kinks = 0: one straight run. */
   int32_t lut_linear;
   float lut_base[4];
   float lut_slope[4];
+  int32_t lut_kinks;
+  float lut_kink_x[ISC_MAX_LUT_KINKS];
+  float lut_kink_dslope[ISC_MAX_LUT_KINKS][4];
 } isc_source;
 
 /* Camera in global cell coordinates; basis/tan/aspect precomputed on the

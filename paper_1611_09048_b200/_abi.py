@@ -21,6 +21,7 @@ MAX_SOURCES = 8
 MAX_CLIP_PLANES = 8
 MAX_CHAIN = 8
 LUT_ENTRIES = 256
+MAX_LUT_KINKS = 3
 MAX_RANKS = 64
 IPC_HANDLE_BYTES = 64
 MAX_SWAP_CTAS = 1024
@@ -55,6 +56,9 @@ class Source(C.Structure):
         ("lut_linear", C.c_int32),
         ("lut_base", C.c_float * 4),
         ("lut_slope", C.c_float * 4),
+        ("lut_kinks", C.c_int32),
+        ("lut_kink_x", C.c_float * MAX_LUT_KINKS),
+        ("lut_kink_dslope", (C.c_float * 4) * MAX_LUT_KINKS),
     ]
 
 

@@ -254,30 +254,46 @@ __global__ void __launch_bounds__(kThreads) march_kernel(const __grid_constant__
 // pair -- the same over-sequence as the reference's per-station loop.
 // ET (early termination, alpha_stop < 1): the even lane composites station by
 // station with the stop test after each.
-// Straight RGBA of a transfer function whose LUT is one straight run
-// (isc_source.lut_linear): identical to the LUT lerp, no shared-memory lookup.
-// Returns the PREMULTIPLIED colour; a non-finite value gets alpha 0 (and so
-// rgb 0) through a select instead of a branch.
+// Straight RGBA of a transfer function whose LUT lerp is piecewise linear
+// with L-1 slope changes (isc_source.lut_linear / lut_kinks):
+//   base + slope*x + sum_k dslope_k * max(x - x_k, 0),
+// identical to the LUT lerp, no shared-memory lookup (the coefficients are
+// kernel-parameter constants, free FFMA operands).  Returns the
+// PREMULTIPLIED colour; a non-finite value gets alpha 0 (and so rgb 0)
+// through a select instead of a branch.
+template <int L>
 __device__ __forceinline__ float4 classify_line_premul(const isc_source& s, float lo, float inv_span, float v) {
   const float x = fminf(fmaxf((v - lo) * inv_span, 0.0f), 1.0f) * (float)(ISC_LUT_ENTRIES - 1);
-  const float a = isfinite(v) ? fmaf(s.lut_slope[3], x, s.lut_base[3]) : 0.0f;
-  return make_float4(fmaf(s.lut_slope[0], x, s.lut_base[0]) * a, fmaf(s.lut_slope[1], x, s.lut_base[1]) * a,
-                     fmaf(s.lut_slope[2], x, s.lut_base[2]) * a, a);
+  float c[4];
+#pragma unroll
+  for (int ch = 0; ch < 4; ++ch) c[ch] = fmaf(s.lut_slope[ch], x, s.lut_base[ch]);
+#pragma unroll
+  for (int k = 0; k < L - 1; ++k) {
+    const float h = fmaxf(x - s.lut_kink_x[k], 0.0f);
+#pragma unroll
+    for (int ch = 0; ch < 4; ++ch) c[ch] = fmaf(s.lut_kink_dslope[k][ch], h, c[ch]);
+  }
+  const float a = isfinite(v) ? c[3] : 0.0f;
+  return make_float4(c[0] * a, c[1] * a, c[2] * a, a);
 }
 
 #ifndef ISC_FAST_MINB
 #define ISC_FAST_MINB 4  // <= 64 registers: 4 CTAs (32 warps) per SM
 #endif
-template <bool INTERP, bool GUARDED, bool PAIRED, bool LINE = false, int DIM = 1, bool ET = false,
+// LINE: 0 = transfer function read from the shared-memory LUT, L >= 1 =
+// analytic piecewise-linear form with L-1 kinks (classify_line_premul<L>).
+template <bool INTERP, bool GUARDED, bool PAIRED, int LINE = 0, int DIM = 1, bool ET = false,
           typename T = float>
 __global__ void __launch_bounds__(kThreads, ISC_FAST_MINB) march_fast_kernel(const __grid_constant__ isc_render_args a,
                                                               const FastField F, int tiles_x, int tiles_y,
                                                               int super_x, int n_codes, int row_order,
                                                               int tw_log2, int tile_x0, int tile_y0) {
   __shared__ float4 lut_s[ISC_LUT_ENTRIES];
-  for (int i = threadIdx.x; i < ISC_LUT_ENTRIES; i += blockDim.x)
-    lut_s[i] = reinterpret_cast<const float4*>(a.src[0].lut)[i];
-  __syncthreads();
+  if (LINE == 0 || !PAIRED) {
+    for (int i = threadIdx.x; i < ISC_LUT_ENTRIES; i += blockDim.x)
+      lut_s[i] = reinterpret_cast<const float4*>(a.src[0].lut)[i];
+    __syncthreads();
+  }
 
   const int lane = threadIdx.x & 31;
   const isc_source& s = a.src[0];
@@ -391,7 +407,8 @@ __global__ void __launch_bounds__(kThreads, ISC_FAST_MINB) march_fast_kernel(con
             fast_gather<DIM, T>(F, p0, vv);
             s0 = run_chain_fast<DIM>(s, vv);
           }
-          c = LINE ? classify_line_premul(s, lo, inv, s0) : premultiply(classify(lut_s, lo, inv, s0));
+          if constexpr (LINE > 0) c = classify_line_premul<LINE>(s, lo, inv, s0);
+          else c = premultiply(classify(lut_s, lo, inv, s0));
         }
         // Only the even lane's accumulator is used (it writes the pixel), so
         // it takes the odd lane's sample with a shuffle-down and composites
@@ -578,7 +595,7 @@ static bool fast_eligible(const isc_render_args* a, FastField& F) {
 }
 
 
-template <bool INTERP, bool GUARDED, bool PAIRED, bool LINE = false, int DIM = 1, bool ET = false,
+template <bool INTERP, bool GUARDED, bool PAIRED, int LINE = 0, int DIM = 1, bool ET = false,
           typename T = float>
 static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_t st) {
   static const int tw_env = getenv("ISC_TILE_W") ? __builtin_ctz(atoi(getenv("ISC_TILE_W"))) : -1;
@@ -597,8 +614,8 @@ static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   OccupancyTuner::Choice ch{cap_env, tw_env >= 0 ? tw_env : 3};
   if (!cap_env && tw_env < 0 && !no_tune && PAIRED) {
-    const int variant = (INTERP ? 1 : 0) | (GUARDED ? 2 : 0) | (LINE ? 4 : 0) | (ET ? 8 : 0) | (DIM << 4) |
-                        ((int)sizeof(T) << 8);
+    const int variant = (INTERP ? 1 : 0) | (GUARDED ? 2 : 0) | (ET ? 8 : 0) | (DIM << 4) | ((int)sizeof(T) << 8) |
+                        (LINE << 12);
     ch = tuner().choose(OccupancyTuner::make_key(a, variant), st, &ev0, &ev1);
   }
   const int tw_log2 = ch.tw_log2;
@@ -631,6 +648,22 @@ static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_
   return ISC_OK;
 }
 
+// Guarded trilinear paired march with the analytic transfer function of
+// `lines` pieces when this instantiation covers it (lines <= MAXL), else the
+// shared-memory LUT.  MAXL bounds the template instantiations per variant.
+template <int MAXL, int DIM, bool ET, typename T>
+static int launch_line(int lines, const isc_render_args* a, const FastField& F, cudaStream_t st) {
+  if (lines > MAXL) lines = 0;
+  switch (lines) {
+    case 1: return launch_fast<true, true, true, 1, DIM, ET, T>(a, F, st);
+    case 2: if constexpr (MAXL >= 2) return launch_fast<true, true, true, 2, DIM, ET, T>(a, F, st); break;
+    case 3: if constexpr (MAXL >= 3) return launch_fast<true, true, true, 3, DIM, ET, T>(a, F, st); break;
+    case 4: if constexpr (MAXL >= 4) return launch_fast<true, true, true, 4, DIM, ET, T>(a, F, st); break;
+    default: break;
+  }
+  return launch_fast<true, true, true, 0, DIM, ET, T>(a, F, st);
+}
+
 extern "C" int isc_render_local(const isc_render_args* a, void* stream) {
   int st = validate(a, true);
   if (st != ISC_OK) return st;
@@ -645,37 +678,22 @@ extern "C" int isc_render_local(const isc_render_args* a, void* stream) {
     const bool guarded = interp && a->src[0].has_guard;
     static const bool no_pair = getenv("ISC_DISABLE_PAIRED") != nullptr;
     const bool paired = !no_pair && a->alpha_stop >= 1.0;
-    const bool line = a->src[0].lut_linear != 0;
+    // analytic transfer function: LINE = 1 + kinks (0 = shared-memory LUT)
+    const int lines = a->src[0].lut_linear != 0 ? 1 + a->src[0].lut_kinks : 0;
+    const bool et = a->alpha_stop < 1.0;
     if (a->src[0].dtype != ISC_F32) {  // double / __half / __nv_bfloat16 scalar fields (fast_eligible)
-      const bool et = a->alpha_stop < 1.0;
-      if (a->src[0].dtype == ISC_F64) {
-        if (et) return line ? launch_fast<true, true, true, true, 1, true, double>(a, F, s)
-                            : launch_fast<true, true, true, false, 1, true, double>(a, F, s);
-        return line ? launch_fast<true, true, true, true, 1, false, double>(a, F, s)
-                    : launch_fast<true, true, true, false, 1, false, double>(a, F, s);
-      }
-      if (a->src[0].dtype == ISC_F16) {
-        if (et) return line ? launch_fast<true, true, true, true, 1, true, __half>(a, F, s)
-                            : launch_fast<true, true, true, false, 1, true, __half>(a, F, s);
-        return line ? launch_fast<true, true, true, true, 1, false, __half>(a, F, s)
-                    : launch_fast<true, true, true, false, 1, false, __half>(a, F, s);
-      }
-      if (et) return line ? launch_fast<true, true, true, true, 1, true, __nv_bfloat16>(a, F, s)
-                          : launch_fast<true, true, true, false, 1, true, __nv_bfloat16>(a, F, s);
-      return line ? launch_fast<true, true, true, true, 1, false, __nv_bfloat16>(a, F, s)
-                  : launch_fast<true, true, true, false, 1, false, __nv_bfloat16>(a, F, s);
+      if (a->src[0].dtype == ISC_F64)
+        return et ? launch_line<1, 1, true, double>(lines, a, F, s) : launch_line<1, 1, false, double>(lines, a, F, s);
+      if (a->src[0].dtype == ISC_F16)
+        return et ? launch_line<1, 1, true, __half>(lines, a, F, s) : launch_line<1, 1, false, __half>(lines, a, F, s);
+      return et ? launch_line<1, 1, true, __nv_bfloat16>(lines, a, F, s)
+                : launch_line<1, 1, false, __nv_bfloat16>(lines, a, F, s);
     }
-    if (a->src[0].feature_dim == 3) {
-      if (a->alpha_stop < 1.0)
-        return line ? launch_fast<true, true, true, true, 3, true>(a, F, s)
-                    : launch_fast<true, true, true, false, 3, true>(a, F, s);
-      return line ? launch_fast<true, true, true, true, 3>(a, F, s) : launch_fast<true, true, true, false, 3>(a, F, s);
-    }
+    if (a->src[0].feature_dim == 3)
+      return et ? launch_line<2, 3, true, float>(lines, a, F, s) : launch_line<2, 3, false, float>(lines, a, F, s);
     // early termination, guarded trilinear: paired with the per-station stop test
-    if (interp && guarded && !no_pair && a->alpha_stop < 1.0)
-      return line ? launch_fast<true, true, true, true, 1, true>(a, F, s)
-                  : launch_fast<true, true, true, false, 1, true>(a, F, s);
-    if (interp && guarded && paired && line) return launch_fast<true, true, true, true>(a, F, s);
+    if (interp && guarded && !no_pair && et) return launch_line<4, 1, true, float>(lines, a, F, s);
+    if (interp && guarded && paired) return launch_line<4, 1, false, float>(lines, a, F, s);
     if (interp && guarded) return paired ? launch_fast<true, true, true>(a, F, s) : launch_fast<true, true, false>(a, F, s);
     if (interp) return paired ? launch_fast<true, false, true>(a, F, s) : launch_fast<true, false, false>(a, F, s);
     return paired ? launch_fast<false, false, true>(a, F, s) : launch_fast<false, false, false>(a, F, s);

@@ -192,11 +192,16 @@ def pack_render_args(domain, volume, scene: SceneState, plans: Sequence[SourcePl
         lut = LUTS.get(plan.tf.lut, device)
         keep.append(lut)
         s.lut = ptr(lut)
-        line = lut_line(plan.tf.lut) if analytic_lut else None
-        if line is not None:
+        pw = lut_analytic(plan.tf.lut) if analytic_lut else None
+        if pw is not None:
+            base, slope, kinks = pw
             s.lut_linear = 1
-            s.lut_base[:] = [float(v) for v in line[0]]
-            s.lut_slope[:] = [float(v) for v in line[1]]
+            s.lut_base[:] = [float(v) for v in base]
+            s.lut_slope[:] = [float(v) for v in slope]
+            s.lut_kinks = len(kinks)
+            for k, (xk, d) in enumerate(kinks):
+                s.lut_kink_x[k] = xk
+                s.lut_kink_dslope[k][:] = [float(v) for v in d]
         prog = device_program(plan.chain)
         s.n_steps = len(prog)
         for j, (op, in_dim, arg) in enumerate(prog):
@@ -270,16 +275,22 @@ _LINE_CACHE: dict = {}
 _LINE_LOCK = threading.Lock()
 
 
-def lut_line(lut: np.ndarray, tol: float = 1e-12):
-    """(base, slope) if all 256 LUT entries lie on one line in x = 0..255
-    (so the LUT lerp equals base + slope * x), else None.  Memoised on the LUT
-    bytes (a transfer function changes only when steered)."""
+def lut_analytic(lut: np.ndarray, max_kinks: int = _abi.MAX_LUT_KINKS, tol: float = 1e-12):
+    """(base, slope, kinks) when the LUT lerp -- the piecewise-linear
+    interpolant through (i, lut[i]), scene.py:139-152 -- changes slope at no
+    more than ``max_kinks`` integer positions: then for x in [0, 255]
+    lerp(x) = base + slope*x + sum_k dslope_k * max(x - x_k, 0) exactly
+    (``kinks`` = [(x_k, dslope_k)]).  None otherwise (the kernel reads the LUT
+    from shared memory).  A tf_from_points ramp with c control points has at
+    most 2(c-2) kinks (one per interior point on an integer position, two
+    when it falls between LUT samples).  Memoised on the LUT bytes (a
+    transfer function changes only when steered)."""
     lut = np.asarray(lut, dtype=np.float64)
-    key = (lut.tobytes(), tol)
+    key = (lut.tobytes(), max_kinks, tol)
     with _LINE_LOCK:
         if key in _LINE_CACHE:
             return _LINE_CACHE[key]
-    res = _lut_line(lut, tol)
+    res = _lut_analytic(lut, max_kinks, tol)
     with _LINE_LOCK:
         if len(_LINE_CACHE) > 256:
             _LINE_CACHE.clear()
@@ -287,16 +298,32 @@ def lut_line(lut: np.ndarray, tol: float = 1e-12):
     return res
 
 
-def _lut_line(lut: np.ndarray, tol: float):
-    second = lut[2:] - 2.0 * lut[1:-1] + lut[:-2]
-    if np.abs(second).max() > tol:
+def _lut_analytic(lut: np.ndarray, max_kinks: int, tol: float):
+    seg = lut[1:] - lut[:-1]                       # slope of segment i = [i, i+1]
+    change = np.abs(seg[1:] - seg[:-1]).max(axis=1) > tol
+    at = np.nonzero(change)[0] + 1                 # segment i starts a new slope
+    if at.size > max_kinks:
         return None
-    slope = (lut[-1] - lut[0]) / (lut.shape[0] - 1)
-    base = lut[0]
-    fit = base[None, :] + slope[None, :] * np.arange(lut.shape[0])[:, None]
+    base, slope = lut[0].copy(), seg[0].copy()
+    kinks = [(float(i), seg[i] - seg[i - 1]) for i in at]
+    x = np.arange(lut.shape[0], dtype=np.float64)[:, None]
+    fit = base[None, :] + slope[None, :] * x
+    for xk, d in kinks:
+        fit = fit + d[None, :] * np.maximum(x - xk, 0.0)
     if np.abs(fit - lut).max() > 1e-9:
         return None
-    return base, slope
+    return base, slope, kinks
+
+
+def lut_line(lut: np.ndarray, tol: float = 1e-12):
+    """(base, slope) if all 256 LUT entries lie on one straight run, else None."""
+    res = lut_analytic(lut, 0, tol)
+    return None if res is None else res[:2]
+
+
+# analytic LUT forms instantiated per (element type, dim, early termination):
+# LINE = 1 + kinks (march.cu dispatch_line)
+_LINE_MAX = {("float", 1, False): 4, ("float", 1, True): 4, ("float", 3, False): 2, ("float", 3, True): 2}
 
 
 def describe_kernel(plans: Sequence[SourcePlan], settings, analytic_lut: bool = True) -> str:
@@ -312,12 +339,17 @@ def describe_kernel(plans: Sequence[SourcePlan], settings, analytic_lut: bool = 
         dtype = getattr(arr, "dtype", None)
         f32 = dtype in (_t.float32, np.float32)
         guarded = interp and p.handle.descriptor.has_guard
-        line = analytic_lut and lut_line(p.tf.lut) is not None
+        pw = lut_analytic(p.tf.lut) if analytic_lut else None
         if (dim == 1 and (f32 or guarded)) or (dim == 3 and f32 and guarded):
             elem = {_t.float32: "float", _t.float64: "double", _t.float16: "__half",
                     _t.bfloat16: "__nv_bfloat16"}.get(dtype, "float")
+            line = 0
+            if pw is not None and guarded:
+                line = 1 + len(pw[2])
+                if line > _LINE_MAX.get((elem, dim, bool(et)), 1):
+                    line = 0
             return (f"isc::march_fast_kernel<INTERP={int(interp)},GUARDED={int(guarded)},PAIRED=1,"
-                    f"LINE={int(line and guarded)},DIM={dim},ET={int(et)},T={elem}>")
+                    f"LINE={line},DIM={dim},ET={int(et)},T={elem}>")
     if 1 <= len(plans) <= 4:
         dims = [p.handle.descriptor.feature_dim for p in plans]
         if interp and all(p.handle.descriptor.has_guard for p in plans) and len(plans) <= 2 and \

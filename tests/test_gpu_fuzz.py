@@ -26,8 +26,13 @@ def _random_case(rng):
         chain = str(rng.choice(CHAINS_VEC if dim == 3 else CHAINS_SCALAR))
         iso = (i == 0 and rng.random() < 0.4 and dim == 1)
         pts = [(0.0, *rng.random(4)), (float(rng.uniform(0.2, 0.8)), *rng.random(4)), (1.0, *rng.random(4))]
-        if rng.random() < 0.3:
+        u = rng.random()
+        if u < 0.3:
             pts = [(0.0, 0.0, 0.0, 0.0, 0.0), (1.0, *rng.random(4))]     # single ramp: analytic path
+        elif u < 0.55:   # 3-4 control points, some on LUT samples: 1-3 kinks (analytic) or more (LUT)
+            mids = sorted(float(int(rng.integers(20, 236)) / 255.0) if rng.random() < 0.5
+                          else float(rng.uniform(0.08, 0.92)) for _ in range(int(rng.integers(1, 3))))
+            pts = [(0.0, *rng.random(4)), *[(t, *rng.random(4)) for t in mids], (1.0, *rng.random(4))]
         srcs.append(dict(dim=dim, chain=chain, mode="iso" if iso else "volume", pts=pts,
                          dtype=str(rng.choice(["float32", "float32", "float16", "float64"])) if ns == 1 else "float32"))
     pos = tuple(float(v) for v in rng.uniform(-2 * n, 3 * n, 3))

@@ -418,6 +418,51 @@ def test_analytic_single_ramp_classification_equals_lut_path():
     assert lut_line(warm.lut) is None
 
 
+@pytest.mark.parametrize("points", [
+    [(0.0, 0.0, 0.1, 0.2, 0.0), (0.6, 0.9, 0.4, 0.1, 0.3), (1.0, 1.0, 1.0, 0.5, 0.8)],       # kink on a sample
+    [(0.0, 0.0, 0.1, 0.2, 0.0), (0.37, 0.9, 0.4, 0.1, 0.3), (1.0, 1.0, 1.0, 0.5, 0.8)],      # between samples
+    [(0.0, 0.0, 0.0, 0.0, 0.0), (0.2, 0.5, 0.1, 0.1, 0.05), (0.6, 0.1, 0.9, 0.3, 0.4), (1.0, 1.0, 1.0, 1.0, 0.9)],
+])
+@pytest.mark.parametrize("alpha_stop", [1.0, 0.95])
+def test_piecewise_linear_tf_classified_analytically(points, alpha_stop):
+    """tf_from_points LUTs with 1-3 slope changes take the analytic hinge form
+    (base + slope x + sum dslope_k max(x - x_k, 0)); images match the
+    shared-memory LUT path and the CPU oracle."""
+    import paper_1611_09048_b200 as P
+    from oracle import isaac_oracle as O
+    from paper_1611_09048_b200.raycast import describe_kernel, lut_analytic
+    torch = _torch()
+    n = 32
+    rng = np.random.default_rng(77)
+    field = rng.random((n + 2,) * 3).astype(np.float32)
+    vol = P.GlobalVolume((n, n, n))
+    dom = vol.local_domain(0, 1)
+    reg = P.SourceRegistry(dom)
+    reg.register_handle(P.array_backed_handle(P.SourceDescriptor("f", 1, has_guard=True),
+                                              torch.from_numpy(field).cuda(), 1))
+    P.update_sources(reg, {0}, {})
+    fr = P.default_registry()
+    ctx = P.RankContext(vol, dom, reg, fr, fr.limits)
+    pos, look = (51.0, 40.0, -30.0), (15.0, 16.0, 17.0)
+    scene = P.SceneState(camera=P.Camera(pos, look, image_size=(80, 60)), tf_points={0: points},
+                         value_ranges={0: (0.1, 0.9)},
+                         settings=P.RenderSettings(active_set=(0,), early_termination_alpha=alpha_stop))
+    pw = lut_analytic(scene.transfer_function(0).lut)
+    assert pw is not None and 1 <= len(pw[2]) <= 3
+    plans = P.build_plans(reg, fr, fr.limits, scene)
+    assert f"LINE={1 + len(pw[2])}" in describe_kernel(plans, scene.settings)
+    fast = P.render_local(ctx, scene).pixels.cpu().numpy()
+    lut = P.render_local(ctx, scene, analytic_lut=False).pixels.cpu().numpy()
+    # identical up to float32 rounding; with early termination a pixel may
+    # stop one station apart where the alpha test sits on the threshold
+    assert np.abs(fast - lut).max() <= (5e-6 if alpha_stop >= 1.0 else RGBA_TOL)
+    src = O.Source(array=field, offset=(0, 0, 0), size=(n, n, n), guard=1, lut=O.lut_from_points(points),
+                   value_range=(0.1, 0.9))
+    ref = O.render_brick({"position": pos, "look_at": look, "width": 80, "height": 60},
+                         O.Brick((0, 0, 0), (n, n, n), 1, (n, n, n)), [src], alpha_stop=alpha_stop)
+    assert np.abs(fast - ref.rgba).max() <= RGBA_TOL
+
+
 @pytest.mark.parametrize("multi", [False, True])
 def test_screen_rect_culling_is_exact(multi):
     """Without per-pixel debug outputs the persistent kernels only schedule
