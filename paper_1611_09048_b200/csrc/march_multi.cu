@@ -527,7 +527,7 @@ __global__ void __launch_bounds__(kThreads, ISC_MULTI_FAST_MINB)
           const float4* lut = lut_s + si * ISC_LUT_ENTRIES;
           const float inv = inv_span[si];
           if (s.mode != ISC_ISO) {
-            st = over4(st, premultiply(classify(lut, s.range_lo, inv, cur)));
+            st = over4(st, classify_src_premul(s, lut, inv, cur));
             continue;
           }
           // ---- iso: raycast.py:384-468 (every source here is guarded: "exact") ----

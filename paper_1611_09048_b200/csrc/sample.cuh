@@ -185,10 +185,15 @@ static __device__ __noinline__ void chain_step_rare(const isc_chain_step& st, fl
 // run_chain (same float32 operations in the same order).  After a reducing
 // step only component 0 is meaningful; the others keep being computed and are
 // ignored.
+// The step loop is unrolled to ISC_MAX_CHAIN so every step's opcode and
+// arguments are read at a compile-time offset of the kernel parameters
+// (immediate constant-bank operands, no indexed constant loads).
 template <int D>
 __device__ __forceinline__ float run_chain_fast(const isc_source& s, float v[4]) {
   bool reduced = (D == 1);
-  for (int i = 0; i < s.n_steps; ++i) {
+#pragma unroll
+  for (int i = 0; i < ISC_MAX_CHAIN; ++i) {
+    if (i >= s.n_steps) break;
     const isc_chain_step& st = s.steps[i];
     const int op = st.op;
     if (op == ISC_OP_ADD) {
@@ -229,6 +234,28 @@ __device__ __forceinline__ float4 classify(const float4* lut, float lo, float in
 
 __device__ __forceinline__ float4 premultiply(float4 c) {
   return make_float4(c.x * c.w, c.y * c.w, c.z * c.w, c.w);
+}
+
+// Premultiplied colour of a source whose transfer function has the analytic
+// piecewise-linear form (isc_source.lut_linear, lut_kinks at run time; see
+// march.cu classify_line_premul for the compile-time variant), else the
+// shared-memory LUT.  Warp-uniform branches.
+__device__ __forceinline__ float4 classify_src_premul(const isc_source& s, const float4* lut, float inv_span,
+                                                     float v) {
+  if (!s.lut_linear) return premultiply(classify(lut, s.range_lo, inv_span, v));
+  const float x = fminf(fmaxf((v - s.range_lo) * inv_span, 0.0f), 1.0f) * (float)(ISC_LUT_ENTRIES - 1);
+  float c[4];
+#pragma unroll
+  for (int ch = 0; ch < 4; ++ch) c[ch] = fmaf(s.lut_slope[ch], x, s.lut_base[ch]);
+#pragma unroll
+  for (int k = 0; k < ISC_MAX_LUT_KINKS; ++k) {
+    if (k >= s.lut_kinks) break;
+    const float h = fmaxf(x - s.lut_kink_x[k], 0.0f);
+#pragma unroll
+    for (int ch = 0; ch < 4; ++ch) c[ch] = fmaf(s.lut_kink_dslope[k][ch], h, c[ch]);
+  }
+  const float a = isfinite(v) ? c[3] : 0.0f;
+  return make_float4(c[0] * a, c[1] * a, c[2] * a, a);
 }
 
 }  // namespace isc
