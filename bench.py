@@ -385,10 +385,21 @@ def run_b200(args):
         dist.all_reduce(br)
     peak, peak_src = peak_hbm()
     achieved = float(br.item()) / (kernel_ms_max * 1e-3) / 1e9 / world
-    traffic = None
+    # ncu evidence for this config (profiles/ncu_counters.json, written by
+    # tools/ncu_counters.py from one `ncu --set full` capture of the kernel)
+    traffic, l1tex = None, None
     try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            traffic = json.load(fh).get(f"{args.config}_n{world}")
+        with open(os.path.join(ROOT, "profiles", "ncu_counters.json")) as fh:
+            rec = json.load(fh).get(f"{args.config}_n{world}")
+        if rec:
+            traffic = rec.get("traffic_bytes")
+            l1tex = {"data_pipe_lsu_frac": round(rec["l1tex_data_pipe_lsu_pct"] / 100.0, 4),
+                     "dram_throughput_frac": round(rec["dram_throughput_pct"] / 100.0, 4),
+                     "issue_active_frac": round(rec["issue_active_pct"] / 100.0, 4),
+                     "l1_hit_rate": round(rec["l1_hit_rate_pct"] / 100.0, 4),
+                     "ncu_kernel_ms": round(rec["duration_ms"], 4), "source": rec["source"],
+                     "note": "the gather's real limiter: L1TEX data-pipe (LSU) wavefronts as a fraction of "
+                             "peak, from the ncu capture named in source (cold, serialised launch)"}
     except Exception:
         pass
 
@@ -455,8 +466,8 @@ def run_b200(args):
         P, torch, dist, ctx, scenes[0], transport, canvas, order, rank, world, red_dev, field)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(field, domain, volume, scene, samples_frame, budget_s=args.cpu_budget)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not cfg.get("multi") and not cfg.get("weak"):
+        cpu = cpu_baseline(field.cpu().numpy(), cfg, n, samples_frame, budget_s=args.cpu_budget)
 
     if rank == 0:
         line = {
@@ -473,7 +484,8 @@ def run_b200(args):
             "samples_note": ("samples = stations x active sources; iso rays stop at the hit" if cfg.get("multi")
                              else "samples = stations (one active source)"),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+                         "frac": round(achieved / peak, 4), "traffic": traffic, "l1tex": l1tex,
+                         "peak_source": peak_src,
                          "kernel": describe_kernel(plans[0], scenes[0].settings), "kernel_ms": round(kernel_ms_max, 4),
                          "algorithmic_bytes_per_launch": int(br.item() / world)},
             "e2e": e2e,
@@ -635,140 +647,228 @@ def run_e2e(P, torch, dist, ctx, scene, transport, canvas, order, rank, world, r
 
 
 # --------------------------------------------------------------------------
-# CPU baselines (oracle port; the reference itself is pure Python and cannot
-# travel to the GPU box -- DESIGN.md)
+# CPU baselines.  The reference itself (insitu 0.1.0, pure Python + numpy) is
+# pip-installed into baseline/_ref (git-ignored, it travels to
+# the GPU box with the snapshot) and timed through its own functions:
+# render_local's body (raycast.py:492-541: ray_directions, _ray_box_intervals,
+# _apply_clip_planes, march_rays) restricted to a stated subset of image rows,
+# one worker process per host core.  Without baseline/_ref the oracle port
+# (oracle/isaac_oracle.py, bit-identical to the reference per the goldens)
+# stands in and the line says kind "port".
 
-
-def _frame_rays(n, image):
-    from oracle import isaac_oracle as O
-    pos, look = harness_camera(n)
-    w, h = image
-    return pos, O.primary_rays(pos, look, (0.0, 1.0, 0.0), math.radians(45.0), w, h)
-
-
-def _row_samples(n, image, pos, dirs, step=0.5):
-    """Stations per image row for the full volume (oracle ray setup only)."""
-    from oracle import isaac_oracle as O
-    w, h = image
-    o = O.np.asarray(pos)
-    ti, to = O.slab(o, dirs, O.np.zeros(3), O.np.full(3, float(n)))
-    hit = O.hit_mask(ti, to)
-    lo, hi = O.station_range(O.np.where(hit, ti, 0.0), O.np.where(hit, to, 0.0), step)
-    per_px = O.np.where(hit, hi - lo, 0)
-    return per_px.reshape(h, w).sum(axis=1)
-
-
-def _pick_rows(per_row, budget_samples):
-    """Every stride-th image row so the sample spans the whole frame and holds
-    about ``budget_samples`` stations."""
-    rows, tot = [], 0
-    stride = max(1, int(per_row.sum() / max(budget_samples, 1)))
-    for r in range(0, len(per_row), stride):
-        rows.append(r)
-        tot += int(per_row[r])
-    return rows, tot
-
-
-def _oracle_rows(args_tuple):
-    rows, = args_tuple
-    import numpy as np
-    from oracle import isaac_oracle as O
-    g = _WORKER
-    sel = np.concatenate([np.arange(r * g["w"], (r + 1) * g["w"]) for r in rows])
-    res = O.render_rays(g["pos"], g["dirs"][sel], g["brick"], [g["src"]], step=0.5, alpha_stop=1.0, interp=True)
-    return int(res.stations.sum())
-
-
+REF_PATH = os.path.join(ROOT, "baseline", "_ref")
 _WORKER: dict = {}
 
 
-def cpu_baseline(field_t, domain, volume, scene, samples_frame, budget_s=15.0, cores=1):
-    """Oracle (float64 numpy restatement of the reference path) on a bounded
-    sample of image rows of the same workload, timed on the host."""
+def _import_reference():
+    if not os.path.isdir(os.path.join(REF_PATH, "insitu")):
+        return None
+    if REF_PATH not in sys.path:
+        sys.path.insert(0, REF_PATH)
+    try:
+        import insitu.fields as rf
+        import insitu.functors as rfn
+        import insitu.raycast as rr
+        import insitu.scene as rs
+    except Exception as exc:  # noqa: BLE001
+        log(f"[reference] baseline/_ref present but not importable: {exc}")
+        return None
+    return rf, rfn, rr, rs
+
+
+def _ref_scene(rs, cfg, n):
+    """The B200 arm's scene (build_scene) as the reference's own SceneState."""
+    pos, look = harness_camera(n)
+    planes = (rs.clip_plane((n / 2.0,) * 3, (0.3, -0.5, 0.81)),) if cfg.get("clip") else ()
+    linear = [(0.0, 0.0, 0.0, 0.0, 0.0), (1.0, 1.0, 1.0, 1.0, 1.0)]
+    settings = rs.RenderSettings(active_set=(0,), interpolation=True, step_length=0.5, early_termination_alpha=1.0)
+    return rs.SceneState(camera=rs.Camera(position=pos, look_at=look, image_size=cfg["image"]),
+                         tf_points={0: linear}, value_ranges={0: (-0.4, 2.4)}, chain_texts={0: ""},
+                         settings=settings, clip_planes=planes)
+
+
+def _setup_cpu_workload(field, n, cfg, kind):
+    """Everything a worker needs, built once in the parent (inherited by fork):
+    the host field, the frame's rays, per-row station counts."""
     import numpy as np
-    from oracle import isaac_oracle as O
-    n = volume.size[0]
-    image = scene.camera.image_size
-    arr = field_t.cpu().numpy() if hasattr(field_t, "cpu") else field_t
-    pos, dirs = _frame_rays(n, image)
-    per_row = _row_samples(n, image, pos, dirs)
-    rate_guess = 1.5e6 * cores
-    rows, expect = _pick_rows(per_row, int(rate_guess * budget_s))
-    src = O.Source(array=arr, offset=domain.offset, size=domain.size, guard=domain.guard_width,
-                   lut=O.lut_from_points([(0, 0, 0, 0, 0), (1, 1, 1, 1, 1)]), value_range=(-0.4, 2.4))
-    brick = O.Brick(domain.offset, domain.size, domain.guard_width, volume.size, volume.decomposition)
-    _WORKER.update(pos=pos, dirs=dirs, w=image[0], brick=brick, src=src)
-    t0 = time.perf_counter()
-    if cores == 1:
-        done = _oracle_rows((rows,))
+    w, h = cfg["image"]
+    g = {"kind": kind, "w": w, "n": n}
+    if kind == "reference":
+        rf, rfn, rr, rs = _import_reference()
+        vol = rf.GlobalVolume((n, n, n), (1, 1, 1))
+        dom = vol.local_domain(0, 1)
+        reg = rf.SourceRegistry(dom)
+        reg.register_handle(rf.array_backed_handle(rf.SourceDescriptor("density", 1, has_guard=True), field, 1))
+        rf.update_sources(reg, {0}, {})
+        scene = _ref_scene(rs, cfg, n)
+        fr = rfn.default_registry()
+        plans = rr.build_plans(reg, fr, rfn.ChainLimits(), scene)
+        origin = np.asarray(scene.camera.position, dtype=np.float64)
+        dirs = scene.camera.ray_directions()
+        lo, hi = np.asarray(dom.offset, np.float64), np.asarray(dom.offset, np.float64) + np.asarray(dom.size, np.float64)
+        t0, t1 = rr._apply_clip_planes(origin, dirs, *rr._ray_box_intervals(origin, dirs, lo, hi), scene.clip_planes)
+        g.update(rr=rr, plans=plans, settings=scene.settings, volume=vol, origin=origin, dirs=dirs, lo=lo, hi=hi,
+                 planes=scene.clip_planes)
     else:
-        import multiprocessing as mp
-        chunks = [rows[i::cores * 4] for i in range(cores * 4) if rows[i::cores * 4]]
-        with mp.get_context("fork").Pool(cores) as pool:
-            done = sum(pool.map(_oracle_rows, [(c,) for c in chunks]))
-    dt = time.perf_counter() - t0
-    sps = done / dt
-    fps = sps / samples_frame
-    return {"value": round(fps, 6), "unit": "frames/s", "cores": cores, "kind": "port",
-            "samples_per_s": round(sps, 1),
-            "sample": f"{len(rows)} of {image[1]} image rows ({done} of {samples_frame} samples) of the same "
-                      f"{n}^3 x {image[0]}x{image[1]} frame, oracle/isaac_oracle.py render_rays, {dt:.1f}s"}
+        from oracle import isaac_oracle as O
+        pos, look = harness_camera(n)
+        origin = np.asarray(pos, dtype=np.float64)
+        dirs = O.primary_rays(pos, look, (0.0, 1.0, 0.0), math.radians(45.0), w, h)
+        t0, t1 = O.slab(origin, dirs, np.zeros(3), np.full(3, float(n)))
+        src = O.Source(array=field, offset=(0, 0, 0), size=(n, n, n), guard=1,
+                       lut=O.lut_from_points([(0, 0, 0, 0, 0), (1, 1, 1, 1, 1)]), value_range=(-0.4, 2.4))
+        g.update(O=O, src=src, brick=O.Brick((0, 0, 0), (n, n, n), 1, (n, n, n), (1, 1, 1)), origin=origin,
+                 dirs=dirs)
+    hit = (t1 > np.maximum(t0, 0.0)) & (t1 > 0.0)
+    k_lo = np.ceil(np.maximum(t0, 0.0) / 0.5)
+    k_hi = np.ceil(np.maximum(t1, 0.0) / 0.5)
+    per_px = np.where(hit, k_hi - k_lo, 0).astype(np.int64)
+    g["per_row"] = per_px.reshape(h, w).sum(axis=1)
+    _WORKER.clear()
+    _WORKER.update(g)
+    return g
+
+
+def _rows_worker(rows):
+    """Stations marched for image rows `rows` (in a forked worker)."""
+    import numpy as np
+    g = _WORKER
+    sel = np.concatenate([np.arange(r * g["w"], (r + 1) * g["w"]) for r in rows])
+    dirs = g["dirs"][sel]
+    if g["kind"] == "reference":           # render_local's body, raycast.py:508-541
+        rr = g["rr"]
+        o = g["origin"]
+        t0, t1 = rr._apply_clip_planes(o, dirs, *rr._ray_box_intervals(o, dirs, g["lo"], g["hi"]), g["planes"])
+        g0, g1 = rr._apply_clip_planes(o, dirs, *rr._ray_box_intervals(o, dirs, np.zeros(3),
+                                                                        np.asarray(g["volume"].size, np.float64)),
+                                       g["planes"])
+        hit = (t1 > np.maximum(t0, 0.0)) & (t1 > 0.0)
+        idx = np.nonzero(hit)[0]
+        if not idx.size:
+            return 0
+        _, stations = rr.march_rays(o, dirs[idx], (t0[idx], t1[idx]), (g0[idx], g1[idx]), g["plans"],
+                                    g["settings"], None, volume=g["volume"])
+        return int(stations)
+    res = g["O"].render_rays(g["origin"], dirs, g["brick"], [g["src"]], step=0.5, alpha_stop=1.0, interp=True)
+    return int(res.stations.sum())
+
+
+def _row_sample(per_row, fraction):
+    """Every k-th image row (k = round(1/fraction)): the sample spans the frame."""
+    k = max(1, int(round(1.0 / fraction)))
+    rows = list(range(0, len(per_row), k))
+    return rows, k, int(per_row[rows].sum())
+
+
+def _run_rows(pool, rows, cores):
+    chunks = [rows[i::cores * 2] for i in range(cores * 2) if rows[i::cores * 2]]
+    if pool is None:
+        return sum(_rows_worker(c) for c in chunks)
+    return sum(pool.map(_rows_worker, chunks))
+
+
+def _host_field(n):
+    import torch
+    vol = __import__("paper_1611_09048_b200").GlobalVolume((n, n, n), (1, 1, 1))
+    return make_field_torch(n, vol.local_domain(0, 1), "cpu").numpy()
+
+
+def cpu_baseline(field_np, cfg, n, samples_frame, budget_s=15.0):
+    """The GPU arm's cpu_baseline: the reference (or the port) on all host
+    cores over every k-th image row of the same frame, ~budget_s of CPU time."""
+    import multiprocessing as mp
+    kind = "reference" if _import_reference() is not None else "port"
+    cores = os.cpu_count() or 1
+    g = _setup_cpu_workload(field_np, n, cfg, kind)
+    rate = 1.0e6 * cores      # ~reference samples/s per core (measured 0.7-1.1 M)
+    rows, k, expect = _row_sample(g["per_row"], min(1.0, rate * budget_s / max(samples_frame, 1)))
+    with mp.get_context("fork").Pool(cores) as pool:
+        t0 = time.perf_counter()
+        done = _run_rows(pool, rows, cores)
+        dt = time.perf_counter() - t0
+    frac = done / samples_frame
+    return {"value": round(frac / dt, 6), "unit": "frames/s", "cores": cores, "kind": kind,
+            "samples_per_s": round(done / dt, 1),
+            "sample": f"every {k}-th image row ({len(rows)} of {cfg['image'][1]} rows, {done} of {samples_frame} "
+                      f"samples = {100.0 * frac:.2f}% of the frame) of the same {n}^3 x "
+                      f"{cfg['image'][0]}x{cfg['image'][1]} frame in {dt:.1f}s; value = sampled fraction / time; "
+                      + ("the reference's own render_local body (march_rays) from baseline/_ref"
+                         if kind == "reference" else "oracle/isaac_oracle.py render_rays (port)")}
 
 
 def run_reference(args):
-    """--impl reference: the reference algorithm (oracle port, all host cores)."""
+    """--impl reference: the reference's own CPU path (baseline/_ref, else the
+    oracle port) on all host cores, rank 0 only.  One step = the frame's
+    image rows k, 2k, 3k, ... (a fixed, stated fraction of the frame, sized so
+    --steps K --warmup W ends in a few minutes); value = frames/s = sampled
+    fraction of the frame's samples / measured step time, so ms_per_step x
+    steps is the real timed wall clock."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    import numpy as np
-
-    import paper_1611_09048_b200 as P
-    from oracle import isaac_oracle as O
+    import multiprocessing as mp
     cfg = CONFIGS[args.config]
+    if cfg.get("weak") or cfg.get("multi"):
+        print(json.dumps({"impl": "reference", "unavailable": f"reference arm implemented for the single-source "
+                                                               f"strong-scaling configs (c1, c2, c4), not {args.config}"}))
+        return
     n = cfg["n"]
     w, h = cfg["image"]
-    decomp = DECOMP[world]
-    volume = P.GlobalVolume((n, n, n), (1, 1, 1))
-    domain = volume.local_domain(0, 1)
     cores = os.cpu_count() or 1
-    # host field, same formula as the GPU arm (float32)
+    kind = "reference" if _import_reference() is not None else "port"
     t0 = time.time()
     import torch
     torch.set_num_threads(cores)
-    field = make_field_torch(n, domain, "cpu").numpy()
-    log(f"[reference] host field ready in {time.time() - t0:.1f}s, {cores} cores")
-    scene = build_scene(P, cfg)
-    pos, dirs = _frame_rays(n, cfg["image"])
-    per_row = _row_samples(n, cfg["image"], pos, dirs)
-    samples_frame = int(per_row.sum())
-    src = O.Source(array=field, offset=domain.offset, size=domain.size, guard=1,
-                   lut=O.lut_from_points([(0, 0, 0, 0, 0), (1, 1, 1, 1, 1)]), value_range=(-0.4, 2.4))
-    brick = O.Brick(domain.offset, domain.size, 1, volume.size, volume.decomposition)
-    _WORKER.update(pos=pos, dirs=dirs, w=w, brick=brick, src=src)
-    rows, _ = _pick_rows(per_row, int(1.2e6 * cores * args.ref_step_s))
-    import multiprocessing as mp
-    chunks = [rows[i::cores] for i in range(cores) if rows[i::cores]]
+    field = _host_field(n)
+    g = _setup_cpu_workload(field, n, cfg, kind)
+    samples_frame = int(g["per_row"].sum())
+    log(f"[reference] {kind}: host field + rays ready in {time.time() - t0:.1f}s, {cores} cores")
+    rate = 1.0e6 * cores      # ~reference samples/s per core (measured 0.7-1.1 M)
+    rows, k, expect = _row_sample(g["per_row"], min(1.0, rate * args.ref_step_s / max(samples_frame, 1)))
+    port = None
     with mp.get_context("fork").Pool(cores) as pool:
         for _ in range(args.warmup):
-            pool.map(_oracle_rows, [(c,) for c in chunks])
-        t0 = time.perf_counter()
-        done = 0
+            _run_rows(pool, rows[: max(1, len(rows) // 8)], cores)     # warm the workers (imports, pages)
+        times, done = [], 0
         for _ in range(args.steps):
-            done += sum(pool.map(_oracle_rows, [(c,) for c in chunks]))
-        dt = time.perf_counter() - t0
-    sps = done / dt
-    fps = sps / samples_frame
+            a = time.perf_counter()
+            done += _run_rows(pool, rows, cores)
+            times.append(time.perf_counter() - a)
+    dt = sum(times)
+    per_step = done / args.steps
+    frac = per_step / samples_frame
+    fps = frac / (dt / args.steps)
+    if kind == "reference":   # the port on the same rows, once, for the port/reference speed ratio
+        try:
+            gp = _setup_cpu_workload(field, n, cfg, "port")
+            sub = rows[: max(1, len(rows) // 4)]
+            with mp.get_context("fork").Pool(cores) as pool:
+                a = time.perf_counter()
+                pd = _run_rows(pool, sub, cores)
+                pt = time.perf_counter() - a
+            ref_rate = done / dt
+            port = {"samples_per_s": round(pd / pt, 1), "reference_samples_per_s": round(ref_rate, 1),
+                    "port_over_reference_speed": round((pd / pt) / ref_rate, 3),
+                    "note": "oracle/isaac_oracle.py on a quarter of the same rows, same cores"}
+        except Exception as exc:  # noqa: BLE001
+            port = {"error": str(exc)}
     line = {"metric": METRIC, "value": round(fps, 6), "unit": "frames/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(1000.0 / fps, 1), "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": round(1000.0 * dt / args.steps, 1), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": {"workload": f"{args.config.upper()}: {cfg['desc']}", "volume": [n, n, n], "image": [w, h],
-                       "decomposition": list(decomp), "samples_per_frame": samples_frame},
-            "gsamples_per_s": round(sps / 1e9, 6),
-            "cpu_baseline": {"value": round(fps, 6), "unit": "frames/s", "cores": cores, "kind": "port",
-                             "sample": f"per step {len(rows)} of {h} image rows of the {n}^3 frame "
-                                       f"({done // max(args.steps, 1)} samples), oracle/isaac_oracle.py "
-                                       f"render_rays over {cores} worker processes"},
-            "e2e": {"value": round(fps, 6), "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                       "decomposition": [1, 1, 1], "samples_per_frame": samples_frame,
+                       "step_unit": f"every {k}-th image row of the frame ({len(rows)} rows, {per_step:.0f} samples "
+                                    f"= {100.0 * frac:.2f}% of the frame's samples)"},
+            "gsamples_per_s": round(done / dt / 1e9, 6),
+            "cpu_baseline": {"value": round(fps, 6), "unit": "frames/s", "cores": cores, "kind": kind,
+                             "sample": f"per step every {k}-th image row of the {n}^3 frame, "
+                                       + ("the reference's render_local body (insitu.raycast.march_rays, "
+                                          "baseline/_ref)" if kind == "reference" else
+                                          "oracle/isaac_oracle.py render_rays") + f" over {cores} worker processes"},
+            "e2e": {"value": round(fps, 6), "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "consistency": {"timed_seconds": round(dt, 2), "steps_x_ms_per_step_s": round(dt, 2),
+                            "frames_per_step": round(frac, 5)},
+            "port_check": port}
     print(json.dumps(line), flush=True)
 
 
@@ -781,7 +881,7 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
-    ap.add_argument("--ref-step-s", type=float, default=4.0)
+    ap.add_argument("--ref-step-s", type=float, default=3.0, help="reference arm: target seconds per step")
     ap.add_argument("--share-gpu", action="store_true", help="test only: all ranks on cuda:0")
     ap.add_argument("--no-host-field-e2e", action="store_true")
     ap.add_argument("--dry-run", action="store_true",

@@ -412,9 +412,13 @@ __device__ __forceinline__ bool cell_guard_ok(const MultiField& M, const double 
 #ifndef ISC_MULTI_FAST_MINB
 #define ISC_MULTI_FAST_MINB 2
 #endif
+#ifndef ISC_MULTI_FAST_THREADS
+#define ISC_MULTI_FAST_THREADS 256
+#endif
+constexpr int kMultiFastThreads = ISC_MULTI_FAST_THREADS;
 
 template <int NS, int DIMS>
-__global__ void __launch_bounds__(kThreads, ISC_MULTI_FAST_MINB)
+__global__ void __launch_bounds__(kMultiFastThreads, ISC_MULTI_FAST_MINB)
     march_multi_fast_kernel(const __grid_constant__ isc_render_args a, const __grid_constant__ MultiField M,
                             int tiles_x, int tiles_y, int super_x, int n_codes, int tile_x0, int tile_y0,
                             int tw_log2) {
@@ -615,11 +619,11 @@ static int launch_multi_fast(const isc_render_args* a, const MultiField& M, cuda
   int dev = 0, sms = 148, per_sm = 1;
   ISC_CUDA_CHECK(cudaGetDevice(&dev));
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_multi_fast_kernel<NS, DIMS>, kThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_multi_fast_kernel<NS, DIMS>, kMultiFastThreads, 0);
   int grid = sms * (per_sm > 0 ? per_sm : 1);
-  const int need = (n_codes + (kThreads / 32) - 1) / (kThreads / 32);
+  const int need = (n_codes + (kMultiFastThreads / 32) - 1) / (kMultiFastThreads / 32);
   if (grid > need) grid = need > 0 ? need : 1;
-  march_multi_fast_kernel<NS, DIMS><<<grid, kThreads, 0, st>>>(*a, M, tiles_x, tiles_y, super_x, n_codes, tile_x0,
+  march_multi_fast_kernel<NS, DIMS><<<grid, kMultiFastThreads, 0, st>>>(*a, M, tiles_x, tiles_y, super_x, n_codes, tile_x0,
                                                                 tile_y0, tw_log2);
   ISC_CUDA_CHECK(cudaGetLastError());
   return ISC_OK;

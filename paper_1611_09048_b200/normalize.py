@@ -22,7 +22,7 @@ from .device import as_device_field, dtype_code, ptr, require_cuda, stream_handl
 from .errors import FieldError
 from .functors import FunctorChain, FunctorRegistry, default_registry, device_program, parse_chain
 
-__all__ = ["value_range", "value_range_device", "auto_value_ranges"]
+__all__ = ["value_range", "value_range_device", "reduce_range", "auto_value_ranges"]
 
 
 def _source_struct(array, guard_arr: int, guard_dom: int, feature_dim: int, chain: Optional[FunctorChain],
@@ -72,19 +72,28 @@ def value_range(handle, domain, chain: Optional[FunctorChain] = None, *, group=N
     range.  NaN samples are ignored; (nan, nan) if a brick has no value.
     """
     out = value_range_device(handle, domain, chain, stream=stream)
-    mm = out[:2].clone()
+    lo, hi = out[:2].tolist()
     if group is not None:
-        import torch.distributed as dist
-        g = None if group is True else group
-        lo = torch.where(torch.isnan(mm[:1]), torch.full_like(mm[:1], math.inf), mm[:1])
-        hi = torch.where(torch.isnan(mm[1:]), torch.full_like(mm[1:], -math.inf), mm[1:])
-        dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=g)
-        dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=g)
-        mm = torch.cat([lo, hi])
-        if math.isinf(float(mm[0])) and float(mm[0]) > 0:
-            return (math.nan, math.nan)
-    lo, hi = mm.tolist()
+        return reduce_range(lo, hi, group)
     return (lo, hi)
+
+
+def reduce_range(lo: float, hi: float, group=True):
+    """Global (min, max) over the ranks of ``group`` (True = WORLD) from each
+    rank's brick range; a rank whose brick has no value passes (nan, nan)
+    and is ignored; (nan, nan) if no rank has a value.  One MIN/MAX
+    all-reduce pair on a float32 pair (NCCL on the GPU, gloo on the host)."""
+    import torch.distributed as dist
+    g = None if group is True else group
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(g) == "nccl" else torch.device("cpu")
+    lo_t = torch.tensor([math.inf if math.isnan(lo) else lo], dtype=torch.float32, device=dev)
+    hi_t = torch.tensor([-math.inf if math.isnan(hi) else hi], dtype=torch.float32, device=dev)
+    dist.all_reduce(lo_t, op=dist.ReduceOp.MIN, group=g)
+    dist.all_reduce(hi_t, op=dist.ReduceOp.MAX, group=g)
+    glo, ghi = float(lo_t.item()), float(hi_t.item())
+    if math.isinf(glo) and glo > 0:
+        return (math.nan, math.nan)
+    return (glo, ghi)
 
 
 def auto_value_ranges(scene, rank_ctx, source_ids: Optional[Iterable[int]] = None, *, group=None,

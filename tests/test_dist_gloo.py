@@ -117,3 +117,38 @@ def test_bench_gpus_flag_launches_that_many_ranks():
         assert line["n_gpus"] == n and line["ranks_seen"] == n
         assert line["rank_sum"] == n * (n - 1) // 2
         assert line["decomposition"] == decomp
+
+
+def _range_worker(rank, world, port, out_dir, ranges):
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1611_09048_b200.normalize import reduce_range
+    got = reduce_range(*ranges[rank], group=True)
+    with open(os.path.join(out_dir, f"range{rank}.pkl"), "wb") as fh:
+        pickle.dump(got, fh)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("ranges,want", [
+    ([(0.5, 2.0), (-1.25, 0.75), (0.0, 3.5)], (-1.25, 3.5)),
+    ([(float("nan"), float("nan")), (0.25, 0.5), (0.125, 0.375)], (0.125, 0.5)),   # an empty brick
+    ([(float("nan"), float("nan"))] * 3, None),                                      # nothing anywhere
+])
+def test_value_range_group_reduction(tmp_path, ranges, want):
+    """Cross-rank auto range (normalize.value_range(group=...)): every rank
+    gets the global (min, max) of the per-brick ranges, empty bricks ignored,
+    over a 3-rank gloo group."""
+    import math
+    import torch.multiprocessing as mp
+    world = len(ranges)
+    mp.spawn(_range_worker, args=(world, _free_port(), str(tmp_path), ranges), nprocs=world, join=True)
+    for r in range(world):
+        with open(tmp_path / f"range{r}.pkl", "rb") as fh:
+            got = pickle.load(fh)
+        if want is None:
+            assert all(math.isnan(v) for v in got)
+        else:
+            assert got == want
