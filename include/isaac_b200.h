@@ -57,7 +57,8 @@ extern "C" {
 
 #define ISC_ABI_VERSION 3  /* 2: isc_render_args.ray_dirs / ray_intervals, isc_gradient_normals;
                               3: per-slice swap counters, isc_swap_reset, isc_debug_occupy,
-                                 isc_render_args.no_layout, piecewise-linear LUTs (lut_kinks) */
+                                 isc_render_args.no_layout, piecewise-linear LUTs (lut_kinks),
+                                 float64 iso decisions (iso_exact, iso_threshold_d) */
 #define ISC_MAX_SOURCES 8      /* active sources per render                 */
 #define ISC_MAX_CLIP_PLANES 8
 #define ISC_MAX_CHAIN 8        /* ChainLimits.max_length default is 5        */
@@ -97,6 +98,7 @@ typedef struct {
   int32_t op;        /* isc_op                                    */
   int32_t in_dim;    /* dimension entering this step (1..4)       */
   float arg[4];      /* constant, already broadcast (functors.py:191-194) */
+  double arg_d[4];   /* the same constant in float64 (iso_exact sources) */
 } isc_chain_step;
 
 /* One active source: a zero-copy view of an application array laid out
@@ -127,6 +129,14 @@ typedef struct {
   int32_t lut_kinks;
   float lut_kink_x[ISC_MAX_LUT_KINKS];
   float lut_kink_dslope[ISC_MAX_LUT_KINKS][4];
+  /* Iso surfaces decided exactly as the reference: iso_exact = 1 when the
+   * chain is made of add / mul only (a scalar source) -- the kernels then
+   * evaluate this source's trilinear sample and chain in float64 in the
+   * reference's operation order (raycast.py:182-199, functors.py:212-222)
+   * and compare against iso_threshold_d, so every sign test and crossing
+   * fraction tau equals the reference's bit for bit. */
+  double iso_threshold_d;
+  int32_t iso_exact;
 } isc_source;
 
 /* Camera in global cell coordinates; basis/tan/aspect precomputed on the

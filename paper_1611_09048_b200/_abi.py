@@ -36,7 +36,7 @@ REDUCES = {"length", "sum"}
 
 
 class ChainStep(C.Structure):
-    _fields_ = [("op", C.c_int32), ("in_dim", C.c_int32), ("arg", C.c_float * 4)]
+    _fields_ = [("op", C.c_int32), ("in_dim", C.c_int32), ("arg", C.c_float * 4), ("arg_d", C.c_double * 4)]
 
 
 class Source(C.Structure):
@@ -59,6 +59,8 @@ class Source(C.Structure):
         ("lut_kinks", C.c_int32),
         ("lut_kink_x", C.c_float * MAX_LUT_KINKS),
         ("lut_kink_dslope", (C.c_float * 4) * MAX_LUT_KINKS),
+        ("iso_threshold_d", C.c_double),
+        ("iso_exact", C.c_int32),
     ]
 
 

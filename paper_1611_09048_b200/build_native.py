@@ -18,7 +18,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libisaac_b200.so")
-SOURCES = ["abi.cu", "march.cu", "march_multi.cu", "minmax.cu", "composite.cu", "encode.cu", "toy.cu"]
+SOURCES = ["abi.cu", "march.cu", "march_multi.cu", "march_staged.cu", "minmax.cu", "composite.cu", "encode.cu", "toy.cu"]
 HEADERS = ["common.cuh", "raysetup.cuh", "sample.cuh", "march_common.cuh", "launch_tuner.cuh"]
 
 NVCC_FLAGS = [

@@ -254,29 +254,6 @@ __global__ void __launch_bounds__(kThreads) march_kernel(const __grid_constant__
 // pair -- the same over-sequence as the reference's per-station loop.
 // ET (early termination, alpha_stop < 1): the even lane composites station by
 // station with the stop test after each.
-// Straight RGBA of a transfer function whose LUT lerp is piecewise linear
-// with L-1 slope changes (isc_source.lut_linear / lut_kinks):
-//   base + slope*x + sum_k dslope_k * max(x - x_k, 0),
-// identical to the LUT lerp, no shared-memory lookup (the coefficients are
-// kernel-parameter constants, free FFMA operands).  Returns the
-// PREMULTIPLIED colour; a non-finite value gets alpha 0 (and so rgb 0)
-// through a select instead of a branch.
-template <int L>
-__device__ __forceinline__ float4 classify_line_premul(const isc_source& s, float lo, float inv_span, float v) {
-  const float x = fminf(fmaxf((v - lo) * inv_span, 0.0f), 1.0f) * (float)(ISC_LUT_ENTRIES - 1);
-  float c[4];
-#pragma unroll
-  for (int ch = 0; ch < 4; ++ch) c[ch] = fmaf(s.lut_slope[ch], x, s.lut_base[ch]);
-#pragma unroll
-  for (int k = 0; k < L - 1; ++k) {
-    const float h = fmaxf(x - s.lut_kink_x[k], 0.0f);
-#pragma unroll
-    for (int ch = 0; ch < 4; ++ch) c[ch] = fmaf(s.lut_kink_dslope[k][ch], h, c[ch]);
-  }
-  const float a = isfinite(v) ? c[3] : 0.0f;
-  return make_float4(c[0] * a, c[1] * a, c[2] * a, a);
-}
-
 #ifndef ISC_FAST_MINB
 #define ISC_FAST_MINB 4  // <= 64 registers: 4 CTAs (32 warps) per SM
 #endif
@@ -648,6 +625,10 @@ static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_
   return ISC_OK;
 }
 
+namespace isc {
+int launch_staged(int lines, const isc_render_args* a, const FastField& F, cudaStream_t st);  // march_staged.cu
+}
+
 // Guarded trilinear paired march with the analytic transfer function of
 // `lines` pieces when this instantiation covers it (lines <= MAXL), else the
 // shared-memory LUT.  MAXL bounds the template instantiations per variant.
@@ -693,6 +674,8 @@ extern "C" int isc_render_local(const isc_render_args* a, void* stream) {
       return et ? launch_line<2, 3, true, float>(lines, a, F, s) : launch_line<2, 3, false, float>(lines, a, F, s);
     // early termination, guarded trilinear: paired with the per-station stop test
     if (interp && guarded && !no_pair && et) return launch_line<4, 1, true, float>(lines, a, F, s);
+    const bool stage = getenv("ISC_STAGE") != nullptr;  // shared-memory brick staging (march_staged.cu), read per call
+    if (interp && guarded && paired && stage) return isc::launch_staged(lines, a, F, s);
     if (interp && guarded && paired) return launch_line<4, 1, false, float>(lines, a, F, s);
     if (interp && guarded) return paired ? launch_fast<true, true, true>(a, F, s) : launch_fast<true, true, false>(a, F, s);
     if (interp) return paired ? launch_fast<true, false, true>(a, F, s) : launch_fast<true, false, false>(a, F, s);

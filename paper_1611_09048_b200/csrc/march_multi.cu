@@ -97,6 +97,77 @@ __device__ __forceinline__ void cell_of(const double p[3], int& ix, int& iy, int
   fz = (float)dsub(p[2], flz);
 }
 
+// Cell, float32 fractions and the exact float64 fractions (iso_exact sources).
+__device__ __forceinline__ void cell_of_d(const double p[3], int& ix, int& iy, int& iz, double& fxd, double& fyd,
+                                          double& fzd) {
+  const double flx = floor_split(p[0], ix), fly = floor_split(p[1], iy), flz = floor_split(p[2], iz);
+  fxd = dsub(p[0], flx);
+  fyd = dsub(p[1], fly);
+  fzd = dsub(p[2], flz);
+}
+
+// The reference's float64 trilinear (raycast.py:182-199) from the 8 corners
+// (x fastest: v000 v100 v010 v110 v001 v101 v011 v111): out starts at 0 and
+// accumulates ((wx*wy)*wz)*corner over dz, dy, dx in that order, w = f or
+// 1 - f -- the same roundings as numpy, so the value is bit-identical.
+__device__ __forceinline__ double trilinear_d(const float c[8], double fx, double fy, double fz) {
+  double out = 0.0;
+#pragma unroll
+  for (int dz = 0; dz < 2; ++dz) {
+    const double wz = dz ? fz : dsub(1.0, fz);
+#pragma unroll
+    for (int dy = 0; dy < 2; ++dy) {
+      const double wy = dy ? fy : dsub(1.0, fy);
+#pragma unroll
+      for (int dx = 0; dx < 2; ++dx) {
+        const double wx = dx ? fx : dsub(1.0, fx);
+        out = dadd(out, dmul(dmul(dmul(wx, wy), wz), (double)c[dz * 4 + dy * 2 + dx]));
+      }
+    }
+  }
+  return out;
+}
+
+// float64 add / mul chain of an iso_exact source (functors.py:212-222).
+__device__ __forceinline__ double run_chain_d(const isc_source& s, double v) {
+#pragma unroll
+  for (int i = 0; i < ISC_MAX_CHAIN; ++i) {
+    if (i >= s.n_steps) break;
+    const isc_chain_step& st = s.steps[i];
+    v = st.op == ISC_OP_ADD ? dadd(v, st.arg_d[0]) : dmul(v, st.arg_d[0]);
+  }
+  return v;
+}
+
+// The 8 corners of a guarded scalar source at base cell (x0, y0, z0).
+__device__ __forceinline__ void corners_guarded(const MultiSrc& S, int x0, int y0, int z0, float c[8]) {
+  const float* p = S.f + (z0 * S.sz + y0 * S.sy + x0 * S.sx);
+  const int dx = S.sx, dy = S.sy, dz = S.sz;
+  c[0] = __ldg(p);
+  c[1] = __ldg(p + dx);
+  c[2] = __ldg(p + dy);
+  c[3] = __ldg(p + dy + dx);
+  const float* q = p + dz;
+  c[4] = __ldg(q);
+  c[5] = __ldg(q + dx);
+  c[6] = __ldg(q + dy);
+  c[7] = __ldg(q + dy + dx);
+}
+
+// float32 trilinear of 8 corners (the kernels' usual arithmetic).
+__device__ __forceinline__ float lerp8(const float c[8], float fx, float fy, float fz) {
+  const float a0 = fmaf(fx, c[1] - c[0], c[0]), a1 = fmaf(fx, c[3] - c[2], c[2]);
+  const float a2 = fmaf(fx, c[5] - c[4], c[4]), a3 = fmaf(fx, c[7] - c[6], c[6]);
+  const float b0 = fmaf(fy, a1 - a0, a0), b1 = fmaf(fy, a3 - a2, a2);
+  return fmaf(fz, b1 - b0, b0);
+}
+
+// Iso value of source si at a global position, as a double: the exact
+// float64 value for an iso_exact source (guarded), else the float32 chain.
+template <bool INTERP>
+__device__ __noinline__ double iso_point_value(const MultiSrc& S, const MultiField& M, const isc_source& src,
+                                               const double p[3], uint32_t* err);
+
 // Chained scalar of one source at an arbitrary global position (iso extras).
 template <bool INTERP>
 __device__ __noinline__ float point_scalar(const MultiSrc& S, const MultiField& M, const isc_source& src,
@@ -107,6 +178,27 @@ __device__ __noinline__ float point_scalar(const MultiSrc& S, const MultiField& 
   float v[4] = {0.f, 0.f, 0.f, 0.f};
   multi_sample<INTERP>(S, M, ix, iy, iz, fx, fy, fz, v, err);
   return run_chain(src, v, S.dim);
+}
+
+template <bool INTERP>
+__device__ __noinline__ double iso_point_value(const MultiSrc& S, const MultiField& M, const isc_source& src,
+                                               const double p[3], uint32_t* err) {
+  if (INTERP && src.iso_exact && S.guarded && S.dim == 1) {
+    int ix, iy, iz;
+    double fx, fy, fz;
+    cell_of_d(p, ix, iy, iz, fx, fy, fz);
+    int x0 = ix - M.lo[0], y0 = iy - M.lo[1], z0 = iz - M.lo[2];
+    if ((unsigned)x0 > (unsigned)S.hi[0] || (unsigned)y0 > (unsigned)S.hi[1] || (unsigned)z0 > (unsigned)S.hi[2]) {
+      if (err) atomicAdd(err, 1u);
+      x0 = min(max(x0, 0), S.hi[0]);
+      y0 = min(max(y0, 0), S.hi[1]);
+      z0 = min(max(z0, 0), S.hi[2]);
+    }
+    float c[8];
+    corners_guarded(S, x0, y0, z0, c);
+    return run_chain_d(src, trilinear_d(c, fx, fy, fz));
+  }
+  return (double)point_scalar<INTERP>(S, M, src, p, err);
 }
 
 __device__ __forceinline__ bool reach(const double off[3], const double size[3], int g, const double p[3]) {
@@ -150,8 +242,8 @@ __device__ __noinline__ float3 multi_normal(const MultiSrc& S, const MultiField&
 // Rare iso pair tests of source si, out of line (see iso_hit_color): the
 // entry pair's earlier value (station k-1 through the guard) and the forward
 // exit pair (the next brick cannot reach back), raycast.py:384-468.
-__device__ __noinline__ float iso_entry_value(const isc_render_args& a, const MultiField& M, int si, double d0,
-                                              double d1, double d2, int k, uint32_t* err) {
+__device__ __noinline__ double iso_entry_value(const isc_render_args& a, const MultiField& M, int si, double d0,
+                                               double d1, double d2, int k, uint32_t* err) {
   const double d[3] = {d0, d1, d2};
   double off[3], bsz[3], pq[3];
 #pragma unroll
@@ -160,11 +252,11 @@ __device__ __noinline__ float iso_entry_value(const isc_render_args& a, const Mu
     bsz[i] = (double)a.brick_size[i];
   }
   station_pos(a.camera.origin, d, dmul((double)(k - 1), a.step), pq);
-  return reach(off, bsz, M.g, pq) ? point_scalar<true>(M.s[si], M, a.src[si], pq, err) : CUDART_NAN_F;
+  return reach(off, bsz, M.g, pq) ? iso_point_value<true>(M.s[si], M, a.src[si], pq, err) : (double)CUDART_NAN_F;
 }
 
 __device__ __noinline__ bool iso_exit_pair(const isc_render_args& a, const MultiField& M, int si, double d0,
-                                           double d1, double d2, int k, double p0, double p1, double p2, float sb,
+                                           double d1, double d2, int k, double p0, double p1, double p2, double sb,
                                            double* tau, uint32_t* err) {
   const double d[3] = {d0, d1, d2}, p[3] = {p0, p1, p2};
   double off[3], bsz[3], vb[3], pn[3], noff[3];
@@ -179,10 +271,10 @@ __device__ __noinline__ bool iso_exit_pair(const isc_render_args& a, const Multi
     noff[i] = dmul(c, vb[i]);
   }
   if (reach(off, bsz, M.g, pn) && !reach(noff, vb, M.g, p)) {
-    const float sn = point_scalar<true>(M.s[si], M, a.src[si], pn, err) - a.src[si].iso_threshold;
-    if ((sb < 0.f) != (sn < 0.f)) {
-      const float den = sb - sn;
-      *tau = den != 0.f ? (double)(sb / den) : 1.0;
+    const double sn = dsub(iso_point_value<true>(M.s[si], M, a.src[si], pn, err), a.src[si].iso_threshold_d);
+    if ((sb < 0.0) != (sn < 0.0)) {
+      const double den = dsub(sb, sn);
+      *tau = den != 0.0 ? ddiv(sb, den) : 1.0;
       return true;
     }
   }
@@ -499,9 +591,9 @@ __global__ void __launch_bounds__(kMultiFastThreads, ISC_MULTI_FAST_MINB)
     bool hit_behind = false;             // crossing between k-1 and k (back = -1) rather than k and k+1
     float4 hit_front = make_float4(0.f, 0.f, 0.f, 0.f);  // the station's sources in front of it
     if (r.hit) {
-      float prev[NS];
+      double prev[NS];   // previous station's iso value (float64: the reference's sign tests)
 #pragma unroll
-      for (int si = 0; si < NS; ++si) prev[si] = CUDART_NAN_F;
+      for (int si = 0; si < NS; ++si) prev[si] = (double)CUDART_NAN_F;
       double kd = (double)r.k_lo;
       const double kendd = (double)kend;
       for (; kd < kendd; kd = dadd(kd, 1.0)) {
@@ -509,15 +601,29 @@ __global__ void __launch_bounds__(kMultiFastThreads, ISC_MULTI_FAST_MINB)
         double p[3];
         station_pos(o, r.d, dmul(kd, step), p);
         int ix, iy, iz;
-        float fx, fy, fz;
-        cell_of(p, ix, iy, iz, fx, fy, fz);
+        double fxd, fyd, fzd;
+        cell_of_d(p, ix, iy, iz, fxd, fyd, fzd);
+        const float fx = (float)fxd, fy = (float)fyd, fz = (float)fzd;
         const int x0 = ix - M.lo[0], y0 = iy - M.lo[1], z0 = iz - M.lo[2];
         float v[NS][4];
+        float cr[NS][8];   // raw corners of scalar sources (iso_exact float64 path)
         // all gathers of the station first (they are independent)
-        gather_guarded<dim_at<DIMS, 0>()>(M.s[0], x0, y0, z0, fx, fy, fz, v[0]);
-        if constexpr (NS > 1) gather_guarded<dim_at<DIMS, 1>()>(M.s[1], x0, y0, z0, fx, fy, fz, v[1]);
-        if constexpr (NS > 2) gather_guarded<dim_at<DIMS, 2>()>(M.s[2], x0, y0, z0, fx, fy, fz, v[2]);
-        if constexpr (NS > 3) gather_guarded<dim_at<DIMS, 3>()>(M.s[3], x0, y0, z0, fx, fy, fz, v[3]);
+#pragma unroll
+        for (int si = 0; si < NS; ++si) {
+          constexpr int kDims[4] = {dim_at<DIMS, 0>(), dim_at<DIMS, 1>(), dim_at<DIMS, 2>(), dim_at<DIMS, 3>()};
+          if (kDims[si] == 1) {
+            corners_guarded(M.s[si], x0, y0, z0, cr[si]);
+            v[si][0] = lerp8(cr[si], fx, fy, fz);
+          } else if (si == 0) {
+            gather_guarded<dim_at<DIMS, 0>()>(M.s[0], x0, y0, z0, fx, fy, fz, v[0]);
+          } else if (si == 1) {
+            gather_guarded<dim_at<DIMS, 1>()>(M.s[1], x0, y0, z0, fx, fy, fz, v[1]);
+          } else if (si == 2) {
+            gather_guarded<dim_at<DIMS, 2>()>(M.s[2], x0, y0, z0, fx, fy, fz, v[2]);
+          } else {
+            gather_guarded<dim_at<DIMS, 3>()>(M.s[3], x0, y0, z0, fx, fy, fz, v[3]);
+          }
+        }
         float4 st = make_float4(0.f, 0.f, 0.f, 0.f);
         bool stop = false;
 #pragma unroll
@@ -535,17 +641,21 @@ __global__ void __launch_bounds__(kMultiFastThreads, ISC_MULTI_FAST_MINB)
             continue;
           }
           // ---- iso: raycast.py:384-468 (every source here is guarded: "exact") ----
-          const float thr = s.iso_threshold;
-          float before = prev[si];
+          // iso_exact: the value, sign test and tau in the reference's float64
+          constexpr int kDimsI[4] = {dim_at<DIMS, 0>(), dim_at<DIMS, 1>(), dim_at<DIMS, 2>(), dim_at<DIMS, 3>()};
+          double cur_d = (double)cur;
+          if (kDimsI[si] == 1 && s.iso_exact) cur_d = run_chain_d(s, trilinear_d(cr[si], fxd, fyd, fzd));
+          const double thr = s.iso_threshold_d;
+          double before = prev[si];
           const int k = (int)kd;
           if (k == k_lo && k - 1 >= kg_lo)  // entry pair: sample k-1 through the guard
             before = iso_entry_value(a, M, si, r.d[0], r.d[1], r.d[2], k, err);
-          const float sa = before - thr, sb = cur - thr;
-          bool hit = isfinite(sa) && ((sa < 0.f) != (sb < 0.f));
+          const double sa = dsub(before, thr), sb = dsub(cur_d, thr);
+          bool hit = isfinite(sa) && ((sa < 0.0) != (sb < 0.0));
           double tau = 0.0, back = 0.0;
           if (hit) {
-            const float den = sa - sb;
-            tau = den != 0.f ? (double)(sa / den) : 1.0;
+            const double den = dsub(sa, sb);
+            tau = den != 0.0 ? ddiv(sa, den) : 1.0;
             back = -1.0;
           }
           if (!hit && k == k_hi - 1 && k + 1 < kg_hi) {  // exit pair, checked forward
@@ -556,7 +666,7 @@ __global__ void __launch_bounds__(kMultiFastThreads, ISC_MULTI_FAST_MINB)
               hit = true;
             }
           }
-          prev[si] = cur;
+          prev[si] = cur_d;
           if (hit && !stop) {  // later sources of the station sit behind the opaque hit
             hit_si = si;
             hit_k = k;

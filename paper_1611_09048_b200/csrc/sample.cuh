@@ -236,6 +236,29 @@ __device__ __forceinline__ float4 premultiply(float4 c) {
   return make_float4(c.x * c.w, c.y * c.w, c.z * c.w, c.w);
 }
 
+// Straight RGBA of a transfer function whose LUT lerp is piecewise linear
+// with L-1 slope changes (isc_source.lut_linear / lut_kinks):
+//   base + slope*x + sum_k dslope_k * max(x - x_k, 0),
+// identical to the LUT lerp, no shared-memory lookup (the coefficients are
+// kernel-parameter constants, free FFMA operands).  Returns the
+// PREMULTIPLIED colour; a non-finite value gets alpha 0 (and so rgb 0)
+// through a select instead of a branch.
+template <int L>
+__device__ __forceinline__ float4 classify_line_premul(const isc_source& s, float lo, float inv_span, float v) {
+  const float x = fminf(fmaxf((v - lo) * inv_span, 0.0f), 1.0f) * (float)(ISC_LUT_ENTRIES - 1);
+  float c[4];
+#pragma unroll
+  for (int ch = 0; ch < 4; ++ch) c[ch] = fmaf(s.lut_slope[ch], x, s.lut_base[ch]);
+#pragma unroll
+  for (int k = 0; k < L - 1; ++k) {
+    const float h = fmaxf(x - s.lut_kink_x[k], 0.0f);
+#pragma unroll
+    for (int ch = 0; ch < 4; ++ch) c[ch] = fmaf(s.lut_kink_dslope[k][ch], h, c[ch]);
+  }
+  const float a = isfinite(v) ? c[3] : 0.0f;
+  return make_float4(c[0] * a, c[1] * a, c[2] * a, a);
+}
+
 // Premultiplied colour of a source whose transfer function has the analytic
 // piecewise-linear form (isc_source.lut_linear, lut_kinks at run time; see
 // march.cu classify_line_premul for the compile-time variant), else the

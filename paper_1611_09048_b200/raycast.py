@@ -188,6 +188,11 @@ def pack_render_args(domain, volume, scene: SceneState, plans: Sequence[SourcePl
         s.has_guard = 1 if hnd.descriptor.has_guard else 0
         s.mode = _abi.ISO if plan.mode == ISO_MODE else _abi.VOLUME
         s.iso_threshold = float(plan.iso_threshold)
+        s.iso_threshold_d = float(plan.iso_threshold)
+        # float64 iso decisions: scalar sources whose chain is add / mul only
+        # (exactly reproducible in the reference's float64 order)
+        s.iso_exact = 1 if (dim == 1 and all(op in (_abi.OPCODES["add"], _abi.OPCODES["mul"])
+                                             for op, _, _ in device_program(plan.chain))) else 0
         s.range_lo, s.range_hi = (float(v) for v in plan.tf.value_range)
         lut = LUTS.get(plan.tf.lut, device)
         keep.append(lut)
@@ -208,6 +213,7 @@ def pack_render_args(domain, volume, scene: SceneState, plans: Sequence[SourcePl
             s.steps[j].op = op
             s.steps[j].in_dim = in_dim
             s.steps[j].arg[:] = [float(v) for v in arg]
+            s.steps[j].arg_d[:] = [float(v) for v in arg]
     return a
 
 

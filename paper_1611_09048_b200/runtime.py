@@ -3,9 +3,9 @@ binary_swap): scene broadcast -> update_sources ->
 render -> visibility order -> binary swap -> metadata merge -> background
 encode/send on rank 0.
 
-Mirrors ``insitu.runtime`` (runtime.py:36-388) minus steering (the gateway /
-steering control plane is out of scope; a root-side ``steer`` hook can be
-plugged in).  The B200 differences: the frame stays on the device until
+Mirrors ``insitu.runtime`` (runtime.py:36-388), including the root's
+steering fold (``apply_steering`` over the context's inbox; the gateway and
+websocket that fill the inbox are out of scope).  The B200 differences: the frame stays on the device until
 ``to_rgba8`` quantises it there (``isc_to_rgba8``), so 8.3 MB instead of 33 MB
 per 1080p frame crosses PCIe, and that copy runs on a side stream while the
 next frame renders (FrameStreamer overlap, runtime.py:187-249).
@@ -15,9 +15,11 @@ from __future__ import annotations
 
 import base64
 import ctypes as C
+import dataclasses
 import io
 import json
 import logging
+import queue
 import threading
 import time
 from dataclasses import dataclass, field
@@ -30,14 +32,15 @@ from .compositing import binary_swap, visibility_order
 from .errors import ChainError
 from .fields import update_sources
 from .functors import parse_chain
-from .scene import SceneState
+from .scene import Camera, SceneState, clip_plane
 
 log = logging.getLogger(__name__)
+_log = log
 
 RAW_RGBA8 = "raw-rgba8"
 PNG = "png"
 
-__all__ = ["RAW_RGBA8", "PNG", "FrameAborted", "to_rgba8", "encode_frame", "decode_frame", "merge_metadata",
+__all__ = ["RAW_RGBA8", "PNG", "CONTROL_ACTIONS", "SteeringResult", "apply_steering", "FrameAborted", "to_rgba8", "encode_frame", "decode_frame", "merge_metadata",
            "FrameStreamer", "FrameResult", "PipelineContext", "broadcast_scene", "frame_pipeline"]
 
 
@@ -181,6 +184,90 @@ class FrameStreamer:
             self._pending = None
 
 
+CONTROL_ACTIONS = ("pause", "resume", "step", "exit")
+
+
+@dataclass
+class SteeringResult:
+    scene: SceneState
+    controls: list
+    dropped: int = 0
+    unknown: int = 0
+
+
+def _steer_camera(scene, m):
+    cam = scene.camera
+    return scene.bump(camera=Camera(position=tuple(m.get("position", cam.position)),
+                                    look_at=tuple(m.get("look_at", cam.look_at)), up=tuple(m.get("up", cam.up)),
+                                    vertical_fov=float(m.get("vertical_fov", cam.vertical_fov)),
+                                    image_size=cam.image_size))
+
+
+def _steer_keyed(field: str, key: str, value):
+    """Fold for the per-source dict fields of the scene (chain texts,
+    transfer-function points, value ranges): copy, set one entry, bump."""
+    def fold(scene, m):
+        table = dict(getattr(scene, field))
+        table[int(m[key])] = value(m)
+        return scene.bump(**{field: table})
+    return fold
+
+
+# one fold per steering action (runtime.py:129-178): scene -> new scene
+_STEER = {
+    "set_period": lambda sc, m: sc.bump(render_period=max(1, int(m["value"]))),
+    "set_active_sources": lambda sc, m: sc.bump(settings=dataclasses.replace(
+        sc.settings, active_set=tuple(sorted(int(i) for i in m["ids"])))),
+    "set_functor_chain": _steer_keyed("chain_texts", "source_id", lambda m: str(m["text"])),
+    "set_transfer_function": _steer_keyed("tf_points", "source_id",
+                                          lambda m: [tuple(float(v) for v in p) for p in m["points"]]),
+    "set_range": _steer_keyed("value_ranges", "source_id", lambda m: (float(m["min"]), float(m["max"]))),
+    "set_camera": _steer_camera,
+    "set_clip_planes": lambda sc, m: sc.bump(clip_planes=tuple(clip_plane(p["point"], p["normal"])
+                                                               for p in m.get("planes", []))),
+    "set_interpolation": lambda sc, m: sc.bump(settings=dataclasses.replace(sc.settings,
+                                                                            interpolation=bool(m["value"]))),
+}
+
+
+def apply_steering(scene: SceneState, messages: Sequence[object]) -> SteeringResult:
+    """Fold steering messages into the scene in arrival order, last writer
+    wins per field (runtime.py:111-184).  pause / resume / step / exit are
+    returned as control events; malformed messages (bad JSON, not an object,
+    missing or mistyped fields) are dropped and counted; unknown actions are
+    counted and ignored.  The scene lives on the host; what it drives on the
+    device (LUTs, the packed launch block) is re-uploaded only for what a
+    message changed (device.LutCache is keyed by LUT content)."""
+    controls: list = []
+    dropped = unknown = 0
+    for raw in messages:
+        msg = raw
+        if isinstance(raw, (str, bytes)):
+            try:
+                msg = json.loads(raw)
+            except (ValueError, UnicodeDecodeError):
+                dropped += 1
+                continue
+        if not isinstance(msg, dict):
+            dropped += 1
+            continue
+        action = msg.get("action")
+        if action in CONTROL_ACTIONS:
+            controls.append(msg)
+            continue
+        fold = _STEER.get(action)
+        if fold is None:
+            unknown += 1
+            _log.warning("ignoring steering message with unknown action %r", action)
+            continue
+        try:
+            scene = fold(scene, msg)
+        except (KeyError, TypeError, ValueError) as exc:
+            dropped += 1
+            _log.warning("dropping malformed steering message %r: %s", msg, exc)
+    return SteeringResult(scene, controls, dropped, unknown)
+
+
 @dataclass
 class FrameResult:
     step: int
@@ -195,7 +282,11 @@ class FrameResult:
 
 @dataclass
 class PipelineContext:
-    """What one rank carries across frames (runtime.py:262-281, steering omitted)."""
+    """What one rank carries across frames (runtime.py:262-281).  Root only:
+    ``inbox`` receives raw steering messages (folded by apply_steering at the
+    start of each frame), ``error_sink`` gets the abort notice of a frame
+    whose chain no longer parses; ``steer`` is an optional extra hook
+    scene -> (scene, controls) run after the inbox fold."""
 
     transport: object
     global_volume: object
@@ -208,6 +299,18 @@ class PipelineContext:
     metadata_hook: Optional[Callable[[int], dict]] = None
     steer: Optional[Callable[[SceneState], tuple]] = None    # root: scene -> (scene, controls)
     canvas: object = None
+    inbox: "queue.Queue" = dataclasses.field(default_factory=queue.Queue)
+    error_sink: Optional[Callable[[dict], None]] = None
+    steering_dropped: int = 0
+    steering_unknown: int = 0
+
+    def drain_inbox(self) -> list:
+        out = []
+        while True:
+            try:
+                out.append(self.inbox.get_nowait())
+            except queue.Empty:
+                return out
 
     @property
     def rank(self) -> int:
@@ -238,6 +341,8 @@ def broadcast_scene(ctx: PipelineContext, scene: Optional[SceneState] = None, co
         env = json.loads(ctx.transport.broadcast_from_root(None).decode("utf-8"))
     ctx.scene = SceneState.from_json(env["scene"])
     if "abort" in env:
+        if ctx.is_root and getattr(ctx, "error_sink", None) is not None:
+            ctx.error_sink({"type": "error", "error": env["abort"]})
         raise FrameAborted(env["abort"], list(env.get("controls", ())))
     return ctx.scene, list(env.get("controls", ()))
 
@@ -252,8 +357,13 @@ def frame_pipeline(ctx: PipelineContext, frame_payload: dict) -> Optional[FrameR
     if ctx.is_root:
         if ctx.streamer is not None:
             ctx.streamer.wait_previous()
+        steering = apply_steering(ctx.scene, ctx.drain_inbox())
+        ctx.steering_dropped += steering.dropped
+        ctx.steering_unknown += steering.unknown
+        scene, controls = steering.scene, list(steering.controls)
         if ctx.steer is not None:
-            scene, controls = ctx.steer(ctx.scene)
+            scene, more = ctx.steer(scene)
+            controls += list(more)
     try:
         scene, controls = broadcast_scene(ctx, scene, controls)
     except FrameAborted as abort:

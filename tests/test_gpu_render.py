@@ -685,3 +685,41 @@ def test_launch_block_not_cached_for_converted_fields():
     P.update_sources(reg2, {0}, {})
     want = P.render_local(P.RankContext(vol, dom, reg2, fr, fr.limits), scene).pixels.cpu().numpy()
     assert np.array_equal(after, want) and not np.array_equal(after, first)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_staged_gather_is_bit_identical(seed, monkeypatch):
+    """Shared-memory brick staging (march_staged.cu, ISC_STAGE=1) reads the
+    same corner values and does the same arithmetic as the direct gather:
+    images and station totals are bit-identical, including chunks whose box
+    overflows the warp's slice (far camera / long rays fall back to global)."""
+    import paper_1611_09048_b200 as P
+    torch = _torch()
+    rng = np.random.default_rng(900 + seed)
+    n = int(rng.choice([24, 48, 96]))
+    field = torch.from_numpy(rng.random((n + 2,) * 3).astype(np.float32)).cuda()
+    vol = P.GlobalVolume((n, n, n), (2, 1, 1) if seed % 2 else (1, 1, 1))
+    for rank in range(vol.rank_count):
+        dom = vol.local_domain(rank, 1)
+        (ox, oy, oz), (sx, sy, sz) = dom.offset, dom.size
+        reg = P.SourceRegistry(dom)
+        reg.register_handle(P.array_backed_handle(P.SourceDescriptor("f", 1, has_guard=True),
+                                                  field[oz:oz + sz + 2, oy:oy + sy + 2, ox:ox + sx + 2], 1))
+        P.update_sources(reg, {0}, {})
+        fr = P.default_registry()
+        ctx = P.RankContext(vol, dom, reg, fr, fr.limits)
+        pos = tuple(float(v) for v in rng.uniform(-1.5 * n, 2.5 * n, 3))
+        pts = [(0.0, 0.0, 0.0, 0.0, 0.0), (1.0, 1.0, 1.0, 1.0, 1.0)] if seed < 2 else \
+            [(0.0, *rng.random(4)), (0.5, *rng.random(4)), (1.0, *rng.random(4))]
+        scene = P.SceneState(camera=P.Camera(pos, (n / 2.0,) * 3, image_size=(97, 61)), tf_points={0: pts},
+                             value_ranges={0: (0.1, 0.9)},
+                             settings=P.RenderSettings(active_set=(0,), step_length=float(rng.choice([0.5, 0.3])),
+                                                       early_termination_alpha=1.0))
+        for analytic in (True, False):
+            monkeypatch.delenv("ISC_STAGE", raising=False)
+            ref = P.render_local(ctx, scene, analytic_lut=analytic)
+            monkeypatch.setenv("ISC_STAGE", "1")
+            got = P.render_local(ctx, scene, analytic_lut=analytic)
+            monkeypatch.delenv("ISC_STAGE", raising=False)
+            assert torch.equal(got.pixels, ref.pixels), (seed, rank, analytic)
+            assert got.stations == ref.stations

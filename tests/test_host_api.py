@@ -375,3 +375,25 @@ def test_lut_analytic_hinge_form_equals_lut_lerp():
     assert lut_line(P.tf_from_points([(0, 0, 0, 0, 0), (1, 1, 1, 1, 1)], (0, 1)).lut) is not None
     noisy = np.sin(np.linspace(0.0, 3.0, 256))[:, None] * np.ones((1, 4))
     assert lut_analytic(noisy) is None
+
+
+def test_apply_steering_matches_reference_goldens():
+    """runtime.apply_steering folds steering messages exactly as the
+    reference (runtime.py:111-184): same resulting scene (JSON), control
+    events, dropped and unknown counts, on 60 seeded sequences generated by
+    the real reference (tests/golden/make_golden_steering.py)."""
+    import json
+    import logging
+    import paper_1611_09048_b200 as P
+    from paper_1611_09048_b200.runtime import apply_steering
+    import os
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "steering.json")) as fh:
+        gold = json.load(fh)
+    logging.getLogger("paper_1611_09048_b200.runtime").setLevel(logging.ERROR)
+    base = P.SceneState.from_json(gold["base"])
+    for case in gold["cases"]:
+        msgs = [m.encode() if b else m for m, b in zip(case["messages"], case["bytes"])]
+        res = apply_steering(base, msgs)
+        assert json.loads(json.dumps(res.scene.to_json())) == case["scene"]
+        assert res.controls == case["controls"]
+        assert (res.dropped, res.unknown) == (case["dropped"], case["unknown"])
