@@ -723,3 +723,31 @@ def test_staged_gather_is_bit_identical(seed, monkeypatch):
             monkeypatch.delenv("ISC_STAGE", raising=False)
             assert torch.equal(got.pixels, ref.pixels), (seed, rank, analytic)
             assert got.stations == ref.stations
+
+
+def test_composite_user_functor_renders_like_its_expansion():
+    """A user functor registered with device_chain renders exactly like the
+    chain it expands to (same device op program)."""
+    import paper_1611_09048_b200 as P
+    from paper_1611_09048_b200.functors import FunctorDescriptor
+    torch = _torch()
+    n = 20
+    rng = np.random.default_rng(5)
+    vec = torch.from_numpy(rng.random((n + 2,) * 3 + (3,)).astype(np.float32)).cuda()
+    vol = P.GlobalVolume((n, n, n))
+    dom = vol.local_domain(0, 1)
+    reg = P.SourceRegistry(dom)
+    reg.register_handle(P.array_backed_handle(P.SourceDescriptor("v", 3, has_guard=True), vec, 1))
+    P.update_sources(reg, {0}, {})
+    fr = P.default_registry()
+    ev = {d: (lambda v, c: np.sqrt(np.sum((v * c[None, :]) ** 2, axis=1, keepdims=True))) for d in range(1, 5)}
+    fr.register_functor(FunctorDescriptor("scaled_norm", True, lambda d: 1), ev, device_chain="mul($) | length")
+    ctx = P.RankContext(vol, dom, reg, fr, fr.limits)
+    imgs = []
+    for chain in ("scaled_norm(2) | add(0.1)", "mul(2) | length | add(0.1)"):
+        scene = P.SceneState(camera=P.Camera((33.0, 27.0, -19.0), (10.0, 10.0, 10.0), image_size=(40, 30)),
+                             tf_points={0: [(0.0, 0.0, 0.1, 0.2, 0.0), (1.0, 1.0, 0.6, 0.3, 0.5)]},
+                             value_ranges={0: (0.0, 4.0)}, chain_texts={0: chain},
+                             settings=P.RenderSettings(active_set=(0,), early_termination_alpha=1.0))
+        imgs.append(P.render_local(ctx, scene).pixels)
+    assert torch.equal(imgs[0], imgs[1]) and float(imgs[0][..., 3].max()) > 0

@@ -397,3 +397,30 @@ def test_apply_steering_matches_reference_goldens():
         assert json.loads(json.dumps(res.scene.to_json())) == case["scene"]
         assert res.controls == case["controls"]
         assert (res.dropped, res.unknown) == (case["dropped"], case["unknown"])
+
+
+def test_composite_user_functor_lowers_to_device_steps():
+    """A user functor defined by a chain of device steps (register_functor(...,
+    device_chain=...), $ = its constant) lowers inline into the kernel op
+    program; the host evaluators still serve eval_chain."""
+    import numpy as np
+    import pytest
+    import paper_1611_09048_b200 as P
+    from paper_1611_09048_b200 import _abi
+    from paper_1611_09048_b200.functors import FunctorDescriptor, device_program
+    reg = P.default_registry()
+    ev = {d: (lambda v, c: np.sqrt(np.sum((v * c[None, :]) ** 2, axis=1, keepdims=True))) for d in range(1, 5)}
+    reg.register_functor(FunctorDescriptor("scaled_norm", True, lambda d: 1), ev, device_chain="mul($) | length")
+    ch = P.parse_chain("scaled_norm(2) | add(1)", reg, None, 3)
+    prog = device_program(ch)
+    assert [op for op, _, _ in prog] == [_abi.OPCODES["mul"], _abi.OPCODES["length"], _abi.OPCODES["add"]]
+    assert prog[0][2][:3] == (2.0, 2.0, 2.0) and prog[2][1] == 1
+    out = P.eval_chain(ch, P.FieldVector((1.0, 2.0, 2.0)))
+    assert abs(out.components[0] - 7.0) < 1e-12
+    # a wrong domain map is caught when lowering; no device path at all raises
+    reg.register_functor(FunctorDescriptor("bad", False, lambda d: d), {d: ev[d] for d in ev}, device_chain="length")
+    with pytest.raises(P.ChainError):
+        device_program(P.parse_chain("bad", reg, None, 3))
+    reg.register_functor(FunctorDescriptor("host_only", False, lambda d: d), {d: (lambda v, c: v) for d in ev})
+    with pytest.raises(P.ChainError):
+        device_program(P.parse_chain("host_only", reg, None, 2))
