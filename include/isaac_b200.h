@@ -137,6 +137,9 @@ typedef struct {
    * fraction tau equals the reference's bit for bit. */
   double iso_threshold_d;
   int32_t iso_exact;
+  /* steps[i].op packed 4 bits per step (step i in bits 4i..4i+3): the hot
+   * kernels branch on one register instead of holding every step's opcode. */
+  uint32_t step_ops;
 } isc_source;
 
 /* Camera in global cell coordinates; basis/tan/aspect precomputed on the

@@ -61,6 +61,7 @@ class Source(C.Structure):
         ("lut_kink_dslope", (C.c_float * 4) * MAX_LUT_KINKS),
         ("iso_threshold_d", C.c_double),
         ("iso_exact", C.c_int32),
+        ("step_ops", C.c_uint32),
     ]
 
 

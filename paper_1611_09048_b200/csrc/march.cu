@@ -28,6 +28,7 @@
 namespace isc {
 
 bool launch_multi(const isc_render_args* a, cudaStream_t st, int* status);  // march_multi.cu
+bool launch_iso_probe(const isc_render_args* a, cudaStream_t st, int* status);  // march_multi.cu
 
 __device__ __forceinline__ void tile_pixel(int& px, int& py) {
   const int t = threadIdx.x, w = t >> 5, l = t & 31;
@@ -320,8 +321,13 @@ __global__ void __launch_bounds__(kThreads, ISC_FAST_MINB) march_fast_kernel(con
       // the full mask (a per-lane mask costs a MATCH.ANY convergence check per
       // shuffle).  Lanes whose ray is finished contribute transparent samples:
       // over(acc, 0) == acc exactly.
-      const long long k_hi = r.k_hi;
-      const long long n = r.hit ? (k_hi - r.k_lo) : 0;
+      long long k_hi = r.k_hi;
+      if (F.stop_counts && r.hit && in_img) {  // split render: stop before the probe's iso hit
+        const long long q_pix = (long long)py * a.camera.width + px;
+        const long long marched = (long long)F.stop_counts[q_pix] - (F.stop_shade[q_pix].w != 0.f ? 1 : 0);
+        k_hi = min(k_hi, r.k_lo + max(marched, 0LL));
+      }
+      const long long n = r.hit ? max(k_hi - r.k_lo, 0LL) : 0;
       long long nm = n;  // stations this lane pair marches
       bool bad_tail = false;
       // Guard contract checked once per ray: every axis of the station
@@ -453,6 +459,7 @@ __global__ void __launch_bounds__(kThreads, ISC_FAST_MINB) march_fast_kernel(con
       }
     }
     const long long pix = (long long)py * a.camera.width + px;
+    if (F.stop_shade) acc = over4(acc, F.stop_shade[pix]);  // the iso hit behind the marched stations
     reinterpret_cast<float4*>(a.out_rgba)[pix] = acc;
     warp_stations += stations;
     if (a.out_stations) a.out_stations[pix] = stations;
@@ -523,12 +530,15 @@ static int validate(const isc_render_args* a, bool need_rgba) {
     if (src.dtype < ISC_F32 || src.dtype > ISC_BF16) return fail(ISC_E_FIELD, "unsupported dtype");
     if (!(src.range_lo < src.range_hi)) return fail(ISC_E_SCENE, "value range must satisfy min < max");
     int dim = src.feature_dim;
+    uint32_t packed = 0;
     for (int i = 0; i < src.n_steps; ++i) {
       if (src.steps[i].in_dim != dim) return fail(ISC_E_CHAIN, "chain step dimension mismatch");
       const int op = src.steps[i].op;
       if (op < ISC_OP_ADD || op > ISC_OP_MAX) return fail(ISC_E_CHAIN, "unknown chain opcode");
       if (op == ISC_OP_LENGTH || op == ISC_OP_SUM) dim = 1;
+      packed |= (uint32_t)op << (4 * i);
     }
+    if (src.step_ops != packed) return fail(ISC_E_CHAIN, "step_ops does not pack steps[].op (4 bits per step)");
   }
   return ISC_OK;
 }
@@ -558,6 +568,8 @@ static bool fast_eligible(const isc_render_args* a, FastField& F) {
   maxoff += (s.feature_dim - 1) * s.stride[3];
   if (maxoff + s.stride[0] + s.stride[1] + s.stride[2] >= INT32_MAX) return false;
   F.f = s.data;
+  F.stop_counts = nullptr;
+  F.stop_shade = nullptr;
   F.sz = (int)s.stride[0];
   F.sy = (int)s.stride[1];
   F.sx = (int)s.stride[2];
@@ -645,6 +657,70 @@ static int launch_line(int lines, const isc_render_args* a, const FastField& F, 
   return launch_fast<true, true, true, 0, DIM, ET, T>(a, F, st);
 }
 
+// C3-style scenes -- one scalar iso source followed by one volume source,
+// guarded trilinear float32, no early termination -- render in two passes:
+// (1) the iso source alone through the multi-source kernel (exact iso
+// decisions, entry / exit pairs, deferred shading) into scratch: per-pixel
+// stations marched and the shaded hit colour; (2) the volume source alone
+// through the paired single-source kernel, each ray stopping before its hit
+// station (the hit station's later sources sit behind the opaque hit,
+// raycast.py:351-369) and compositing the hit colour behind.  Per ray this is
+// the reference's over-sequence; the volume pass runs at the single-source
+// kernel's speed instead of sharing registers with the iso machinery.
+static bool split_eligible(const isc_render_args* a) {
+  if (getenv("ISC_DISABLE_SPLIT") || a->n_sources != 2 || a->ray_dirs || a->alpha_stop < 1.0 || !a->interpolation ||
+      !a->work_counter)
+    return false;
+  const isc_source &iso = a->src[0], &vol = a->src[1];
+  return iso.mode == ISC_ISO && vol.mode == ISC_VOLUME && iso.feature_dim == 1 && iso.dtype == ISC_F32 &&
+         vol.dtype == ISC_F32 && iso.has_guard && vol.has_guard && (vol.feature_dim == 1 || vol.feature_dim == 3);
+}
+
+static int launch_split(const isc_render_args* a, cudaStream_t s, bool* handled) {
+  *handled = false;
+  isc_render_args vol = *a;
+  vol.src[0] = a->src[1];
+  vol.n_sources = 1;
+  FastField F;
+  if (!fast_eligible(&vol, F)) return ISC_OK;
+  const size_t npx = (size_t)a->camera.width * a->camera.height;
+  // scratch: shaded hits (float4), station counts (u32), the volume pass's tile counter
+  char* scratch = nullptr;
+  const size_t bytes = npx * (sizeof(float4) + sizeof(uint32_t)) + 16;
+  ISC_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes, s));
+  float4* shade = reinterpret_cast<float4*>(scratch);
+  uint32_t* counts = a->out_stations ? a->out_stations : reinterpret_cast<uint32_t*>(scratch + npx * sizeof(float4));
+  uint32_t* counter = reinterpret_cast<uint32_t*>(scratch + npx * (sizeof(float4) + sizeof(uint32_t)));
+  isc_render_args iso = *a;  // pass 1: the iso source alone (debug outputs, stations, errors as asked)
+  iso.n_sources = 1;
+  iso.out_rgba = reinterpret_cast<float*>(shade);
+  iso.out_stations = counts;
+  int status = ISC_OK;
+  *handled = true;
+  if (!launch_iso_probe(&iso, s, &status) && !launch_multi(&iso, s, &status))
+    status = fail(ISC_E_VALUE, "iso probe not launchable");
+  if (status == ISC_OK) {
+    // pass 2: the volume source, stopped at each ray's hit
+    vol.out_stations = nullptr;
+    vol.out_station_total = nullptr;
+    vol.out_hit = nullptr;
+    vol.out_t = nullptr;
+    vol.out_krange = nullptr;
+    vol.work_counter = counter;
+    F.stop_counts = counts;
+    F.stop_shade = shade;
+    const cudaError_t e = cudaMemsetAsync(counter, 0, sizeof(uint32_t), s);
+    if (e != cudaSuccess) status = cuda_fail(e, "cudaMemsetAsync");
+    const int lines = vol.src[0].lut_linear != 0 ? 1 + vol.src[0].lut_kinks : 0;
+    if (status == ISC_OK)
+      status = vol.src[0].feature_dim == 3 ? launch_line<2, 3, false, float>(lines, &vol, F, s)
+                                           : launch_line<4, 1, false, float>(lines, &vol, F, s);
+  }
+  const cudaError_t e = cudaFreeAsync(scratch, s);
+  if (status == ISC_OK && e != cudaSuccess) status = cuda_fail(e, "cudaFreeAsync");
+  return status;
+}
+
 extern "C" int isc_render_local(const isc_render_args* a, void* stream) {
   int st = validate(a, true);
   if (st != ISC_OK) return st;
@@ -680,6 +756,11 @@ extern "C" int isc_render_local(const isc_render_args* a, void* stream) {
     if (interp && guarded) return paired ? launch_fast<true, true, true>(a, F, s) : launch_fast<true, true, false>(a, F, s);
     if (interp) return paired ? launch_fast<true, false, true>(a, F, s) : launch_fast<true, false, false>(a, F, s);
     return paired ? launch_fast<false, false, true>(a, F, s) : launch_fast<false, false, false>(a, F, s);
+  }
+  if (split_eligible(a)) {
+    bool handled = false;
+    const int st_split = launch_split(a, s, &handled);
+    if (handled) return st_split;
   }
   static const bool no_multi = getenv("ISC_DISABLE_MULTI") != nullptr;
   bool layout_free_iso = false;  // march_rays(volume=None) with an iso source: generic kernel only

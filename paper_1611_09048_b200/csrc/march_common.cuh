@@ -21,6 +21,12 @@ struct FastField {
   int lo[3];             // brick offset - guard (global cell of array index 0)
   int hi[3];             // largest legal base index (guarded) / size-1 (clamped)
   int g;
+  // split iso + volume render (march.cu launch_split): the iso probe's
+  // per-pixel station counts and shaded hit colours; a ray marches only the
+  // stations before its iso hit and composites the hit colour behind them.
+  // Null in a plain render.
+  const uint32_t* stop_counts;
+  const float4* stop_shade;
 };
 
 // floor(p) as an exact double and as an int without conversion instructions:

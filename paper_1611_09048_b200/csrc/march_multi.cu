@@ -130,11 +130,12 @@ __device__ __forceinline__ double trilinear_d(const float c[8], double fx, doubl
 
 // float64 add / mul chain of an iso_exact source (functors.py:212-222).
 __device__ __forceinline__ double run_chain_d(const isc_source& s, double v) {
+  const unsigned ops = s.step_ops;
 #pragma unroll
   for (int i = 0; i < ISC_MAX_CHAIN; ++i) {
     if (i >= s.n_steps) break;
     const isc_chain_step& st = s.steps[i];
-    v = st.op == ISC_OP_ADD ? dadd(v, st.arg_d[0]) : dmul(v, st.arg_d[0]);
+    v = ((ops >> (4 * i)) & 0xFu) == ISC_OP_ADD ? dadd(v, st.arg_d[0]) : dmul(v, st.arg_d[0]);
   }
   return v;
 }
@@ -488,6 +489,44 @@ __device__ __forceinline__ void gather_guarded(const MultiSrc& S, int x0, int y0
   }
 }
 
+// Standard zero-copy layout (x contiguous, components interleaved: sx ==
+// D, sc == 1 -- a C-contiguous (z, y, x[, c]) array): one 64-bit base per
+// (y, z) corner row, the x+1 corner and every component at an immediate
+// offset (the general form computes a 64-bit address per corner and
+// component from the runtime strides).
+template <int D>
+__device__ __forceinline__ void gather_contig(const MultiSrc& S, int x0, int y0, int z0, float fx, float fy,
+                                              float fz, float v[4]) {
+  const float* r00 = S.f + (z0 * S.sz + y0 * S.sy + x0 * D);
+  const float* r10 = r00 + S.sy;
+  const float* r01 = r00 + S.sz;
+  const float* r11 = r01 + S.sy;
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    const float v000 = __ldg(r00 + c), v100 = __ldg(r00 + D + c), v010 = __ldg(r10 + c), v110 = __ldg(r10 + D + c);
+    const float v001 = __ldg(r01 + c), v101 = __ldg(r01 + D + c), v011 = __ldg(r11 + c), v111 = __ldg(r11 + D + c);
+    const float a0 = fmaf(fx, v100 - v000, v000), a1 = fmaf(fx, v110 - v010, v010);
+    const float a2 = fmaf(fx, v101 - v001, v001), a3 = fmaf(fx, v111 - v011, v011);
+    const float b0 = fmaf(fy, a1 - a0, a0), b1 = fmaf(fy, a3 - a2, a2);
+    v[c] = fmaf(fz, b1 - b0, b0);
+  }
+}
+
+__device__ __forceinline__ void corners_contig(const MultiSrc& S, int x0, int y0, int z0, float c[8]) {
+  const float* r00 = S.f + (z0 * S.sz + y0 * S.sy + x0);
+  const float* r10 = r00 + S.sy;
+  const float* r01 = r00 + S.sz;
+  const float* r11 = r01 + S.sy;
+  c[0] = __ldg(r00);
+  c[1] = __ldg(r00 + 1);
+  c[2] = __ldg(r10);
+  c[3] = __ldg(r10 + 1);
+  c[4] = __ldg(r01);
+  c[5] = __ldg(r01 + 1);
+  c[6] = __ldg(r11);
+  c[7] = __ldg(r11 + 1);
+}
+
 __device__ __forceinline__ bool cell_guard_ok(const MultiField& M, const double p[3]) {
   int ix, iy, iz;
   floor_split(p[0], ix);
@@ -509,7 +548,7 @@ __device__ __forceinline__ bool cell_guard_ok(const MultiField& M, const double 
 #endif
 constexpr int kMultiFastThreads = ISC_MULTI_FAST_THREADS;
 
-template <int NS, int DIMS>
+template <int NS, int DIMS, bool CONTIG>
 __global__ void __launch_bounds__(kMultiFastThreads, ISC_MULTI_FAST_MINB)
     march_multi_fast_kernel(const __grid_constant__ isc_render_args a, const __grid_constant__ MultiField M,
                             int tiles_x, int tiles_y, int super_x, int n_codes, int tile_x0, int tile_y0,
@@ -588,6 +627,7 @@ __global__ void __launch_bounds__(kMultiFastThreads, ISC_MULTI_FAST_MINB)
     int hit_si = -1;                     // first iso source hit (shaded after the loop)
     int hit_k = 0;
     double hit_tau = 0.0;
+    double hit_sb = 0.0;                 // backward pairs: s at the hit station (tau after the loop)
     bool hit_behind = false;             // crossing between k-1 and k (back = -1) rather than k and k+1
     float4 hit_front = make_float4(0.f, 0.f, 0.f, 0.f);  // the station's sources in front of it
     if (r.hit) {
@@ -612,8 +652,14 @@ __global__ void __launch_bounds__(kMultiFastThreads, ISC_MULTI_FAST_MINB)
         for (int si = 0; si < NS; ++si) {
           constexpr int kDims[4] = {dim_at<DIMS, 0>(), dim_at<DIMS, 1>(), dim_at<DIMS, 2>(), dim_at<DIMS, 3>()};
           if (kDims[si] == 1) {
-            corners_guarded(M.s[si], x0, y0, z0, cr[si]);
+            if constexpr (CONTIG) corners_contig(M.s[si], x0, y0, z0, cr[si]);
+            else corners_guarded(M.s[si], x0, y0, z0, cr[si]);
             v[si][0] = lerp8(cr[si], fx, fy, fz);
+          } else if constexpr (CONTIG) {
+            if (si == 0) gather_contig<dim_at<DIMS, 0>()>(M.s[0], x0, y0, z0, fx, fy, fz, v[0]);
+            else if (si == 1) gather_contig<dim_at<DIMS, 1>()>(M.s[1], x0, y0, z0, fx, fy, fz, v[1]);
+            else if (si == 2) gather_contig<dim_at<DIMS, 2>()>(M.s[2], x0, y0, z0, fx, fy, fz, v[2]);
+            else gather_contig<dim_at<DIMS, 3>()>(M.s[3], x0, y0, z0, fx, fy, fz, v[3]);
           } else if (si == 0) {
             gather_guarded<dim_at<DIMS, 0>()>(M.s[0], x0, y0, z0, fx, fy, fz, v[0]);
           } else if (si == 1) {
@@ -666,9 +712,8 @@ __global__ void __launch_bounds__(kMultiFastThreads, ISC_MULTI_FAST_MINB)
           const double sa = dsub(before, thr), sb = dsub(cur_d, thr);
           bool hit = isfinite(sa) && ((sa < 0.0) != (sb < 0.0));
           double tau = 0.0, back = 0.0;
-          if (hit) {
-            const double den = dsub(sa, sb);
-            tau = den != 0.0 ? ddiv(sa, den) : 1.0;
+          if (hit) {  // tau = sa / (sa - sb) once, after the loop (hit_sa / hit_den)
+            tau = sa;
             back = -1.0;
           }
           if (!hit && k == k_hi - 1 && k + 1 < kg_hi) {  // exit pair, checked forward
@@ -684,6 +729,7 @@ __global__ void __launch_bounds__(kMultiFastThreads, ISC_MULTI_FAST_MINB)
             hit_si = si;
             hit_k = k;
             hit_tau = tau;
+            hit_sb = sb;
             hit_behind = back != 0.0;
             hit_front = st;
             stop = true;
@@ -704,6 +750,10 @@ __global__ void __launch_bounds__(kMultiFastThreads, ISC_MULTI_FAST_MINB)
     // Shade iso hits after the loop: hits fall in different iterations, so
     // in-loop shading ran once per hitting lane with the rest of the warp idle.
     if (hit_si >= 0) {
+      if (hit_behind) {  // tau = s_prev / (s_prev - s_cur), raycast.py:434-437
+        const double den = dsub(hit_tau, hit_sb);
+        hit_tau = den != 0.0 ? ddiv(hit_tau, den) : 1.0;
+      }
       double ph[3];
       station_pos(o, r.d, dmul((double)hit_k, step), ph);
       const float4 c = iso_hit_color(a, M, hit_si, r.d[0], r.d[1], r.d[2], ph[0], ph[1], ph[2], hit_tau,
@@ -721,7 +771,225 @@ __global__ void __launch_bounds__(kMultiFastThreads, ISC_MULTI_FAST_MINB)
   }
 }
 
-template <int NS, int DIMS>
+static bool build_multi_field(const isc_render_args* a, MultiField& M);
+
+// ---------------------------------------------------------------------------
+// Paired iso probe: pass 1 of the split iso + volume render (march.cu
+// launch_split).  ONE guarded float32 scalar iso source, no early
+// termination.  A warp is 16 rays (8x2 pixels) x 2 station parities as in
+// march_fast_kernel: the even lane tests the pair (k-1, k) for k = k_lo + 2j,
+// the odd lane the pair (k, k+1); the earlier station's value reaches the
+// later lane by a shuffle, in float64 (the multi-source kernel's exact iso
+// decisions: identity chains take the float64 value inside the error band,
+// add / mul chains always).  The ray's first hit in station order ends it
+// (at one station a backward pair wins over the forward exit pair, as in
+// _iso_detect); after the loop the even lane shades the hit (gradient
+// normal, raycast.py:210-242, 351-369) and writes the shaded colour to
+// out_rgba and the stations marched (hit station included) to out_stations.
+template <bool CONTIG>
+__global__ void __launch_bounds__(kThreads, 4)
+    iso_probe_kernel(const __grid_constant__ isc_render_args a, const __grid_constant__ MultiField M, int tiles_x,
+                     int tiles_y, int super_x, int n_codes, int tile_x0, int tile_y0) {
+  const int lane = threadIdx.x & 31, q = lane & 15, parity = lane >> 4;
+  const double* o = a.camera.origin;
+  const double step = a.step;
+  uint32_t* err = a.error_word;
+  const isc_source& s = a.src[0];
+  const MultiSrc& S = M.s[0];
+  const double thr = s.iso_threshold_d;
+  unsigned long long warp_stations = 0;
+  for (;;) {
+    int t = 0;
+    if (lane == 0) t = (int)atomicAdd(a.work_counter, 1u);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t >= n_codes) break;
+    const int sblk = t >> 6, w = t & 63;
+    const int tx = (sblk % super_x) * 8 + morton3(w, 0);
+    const int ty = (sblk / super_x) * 8 + morton3(w, 1);
+    if (tx >= tiles_x || ty >= tiles_y) continue;
+    const int px = (tx + tile_x0) * 8 + (q & 7), py = (ty + tile_y0) * 2 + (q >> 3);
+    const bool in_img = px < a.camera.width && py < a.camera.height;
+    Ray r;
+    if (in_img) {
+      setup_ray(a, px, py, r);
+    } else {
+      r.hit = false;
+      r.k_lo = r.k_hi = r.kg_lo = r.kg_hi = 0;
+    }
+    const long long pix = (long long)py * a.camera.width + px;
+    if (!parity && in_img) {
+      if (a.out_hit) a.out_hit[pix] = r.hit ? 1 : 0;
+      if (a.out_t) {
+        a.out_t[2 * pix] = r.t_in;
+        a.out_t[2 * pix + 1] = r.t_out;
+      }
+      if (a.out_krange)
+        reinterpret_cast<int4*>(a.out_krange)[pix] =
+            make_int4((int)r.k_lo, (int)r.k_hi, (int)r.kg_lo, (int)r.kg_hi);
+    }
+    const int k_lo = (int)r.k_lo, k_hi = (int)r.k_hi, kg_lo = (int)r.kg_lo, kg_hi = (int)r.kg_hi;
+    // guard contract per ray (march_multi_fast_kernel): stations up to kend
+    int kend = k_hi;
+    bool bad_tail = false;
+    if (r.hit && k_hi > k_lo) {
+      double pa[3], pb[3];
+      station_pos(o, r.d, dmul((double)k_lo, step), pa);
+      station_pos(o, r.d, dmul((double)(k_hi - 1), step), pb);
+      if (!cell_guard_ok(M, pa)) {
+        if (err && !parity) atomicAdd(err, 1u);
+        kend = k_lo;
+      } else if (!cell_guard_ok(M, pb)) {
+        int good = k_lo, bad = k_hi - 1;
+        while (bad - good > 1) {
+          const int mid = good + ((bad - good) >> 1);
+          double pm[3];
+          station_pos(o, r.d, dmul((double)mid, step), pm);
+          if (cell_guard_ok(M, pm)) good = mid;
+          else bad = mid;
+        }
+        kend = bad;
+        bad_tail = true;
+      }
+    }
+    const int n = r.hit ? max(kend - k_lo, 0) : 0;
+    const unsigned trips = __reduce_max_sync(0xffffffffu, (unsigned)((n + 1) >> 1));
+    double prev_even = (double)CUDART_NAN_F;   // even lane: value at k - 1
+    int hit_k = -1;
+    double hit_tau = 0.0, hit_cur = 0.0;
+    bool hit_back = false, done = false;
+    uint32_t stations = 0;
+    int kk = k_lo + parity;
+    for (unsigned j = 0; j < trips; ++j, kk += 2) {
+      const bool valid = !done && kk < kend;
+      double cur = (double)CUDART_NAN_F;
+      double p[3] = {0.0, 0.0, 0.0};
+      if (valid) {
+        station_pos(o, r.d, dmul((double)kk, step), p);
+        int ix, iy, iz;
+        double fxd, fyd, fzd;
+        cell_of_d(p, ix, iy, iz, fxd, fyd, fzd);
+        const int x0 = ix - M.lo[0], y0 = iy - M.lo[1], z0 = iz - M.lo[2];
+        float c[8];
+        if constexpr (CONTIG) corners_contig(S, x0, y0, z0, c);
+        else corners_guarded(S, x0, y0, z0, c);
+        float v[4] = {lerp8(c, (float)fxd, (float)fyd, (float)fzd), 0.f, 0.f, 0.f};
+        cur = (double)run_chain_fast<1>(s, v);
+        if (s.iso_exact) {
+          if (s.n_steps == 0) {  // the error band of march_multi_fast_kernel
+            float m = fabsf(c[0]);
+#pragma unroll
+            for (int i = 1; i < 8; ++i) m = fmaxf(m, fabsf(c[i]));
+            if (!(fabs(dsub(cur, thr)) > (double)m * 0x1p-18)) cur = trilinear_d(c, fxd, fyd, fzd);
+          } else {
+            cur = run_chain_d(s, trilinear_d(c, fxd, fyd, fzd));
+          }
+        }
+      }
+      const double from_even = __shfl_up_sync(0xffffffffu, cur, 16);
+      double prev = parity ? from_even : prev_even;
+      if (!parity && valid && kk == k_lo && k_lo - 1 >= kg_lo)  // entry pair through the guard
+        prev = iso_entry_value(a, M, 0, r.d[0], r.d[1], r.d[2], kk, err);
+      // backward pair: keep s_prev (tau's numerator, computed after the loop
+      // from prev and the station's own value); forward exit pair: tau now
+      bool hit = false;
+      double tau = 0.0;   // backward: s_prev; forward: the crossing fraction
+      bool back = false;
+      if (valid) {
+        const double sa = dsub(prev, thr), sb = dsub(cur, thr);
+        hit = isfinite(sa) && ((sa < 0.0) != (sb < 0.0));
+        if (hit) {
+          tau = sa;
+          back = true;
+        } else if (kk == k_hi - 1 && kk + 1 < kg_hi) {  // exit pair, checked forward
+          double tx = 0.0;
+          if (iso_exit_pair(a, M, 0, r.d[0], r.d[1], r.d[2], kk, p[0], p[1], p[2], sb, &tx, err)) {
+            hit = true;
+            tau = tx;
+          }
+        }
+      }
+      // the even lane takes the odd lane's verdict: its station follows
+      const int odd_bits = __shfl_down_sync(0xffffffffu, (valid ? 1 : 0) | (hit ? 2 : 0) | (back ? 4 : 0), 16);
+      const double odd_tau = __shfl_down_sync(0xffffffffu, tau, 16);
+      const double odd_cur = __shfl_down_sync(0xffffffffu, cur, 16);
+      if (!parity && valid) {
+        ++stations;
+        if (hit) {
+          hit_k = kk;
+          hit_tau = tau;
+          hit_back = back;
+          hit_cur = cur;
+          done = true;
+        } else if (odd_bits & 1) {
+          ++stations;
+          if (odd_bits & 2) {
+            hit_k = kk + 1;
+            hit_tau = odd_tau;
+            hit_back = (odd_bits & 4) != 0;
+            hit_cur = odd_cur;
+            done = true;
+          }
+        }
+      }
+      prev_even = odd_cur;
+      done = __shfl_sync(0xffffffffu, done, q) != 0;  // the odd lane follows its pair
+      if (__all_sync(0xffffffffu, done || kk + 2 >= kend)) break;
+    }
+    if (parity || !in_img) continue;
+    if (bad_tail && hit_k < 0 && err) atomicAdd(err, 1u);  // marched into the bad tail
+    float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (hit_k >= 0) {
+      if (hit_back) {  // tau = s_prev / (s_prev - s_cur), raycast.py:434-437
+        const double den = dsub(hit_tau, dsub(hit_cur, thr));
+        hit_tau = den != 0.0 ? ddiv(hit_tau, den) : 1.0;
+      }
+      double ph[3];
+      station_pos(o, r.d, dmul((double)hit_k, step), ph);
+      c = iso_hit_color(a, M, 0, r.d[0], r.d[1], r.d[2], ph[0], ph[1], ph[2], hit_tau, hit_back ? -1.0 : 0.0, err);
+    }
+    reinterpret_cast<float4*>(a.out_rgba)[pix] = c;
+    if (a.out_stations) a.out_stations[pix] = stations;
+    warp_stations += stations;
+  }
+  if (a.out_station_total) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) warp_stations += __shfl_xor_sync(0xffffffffu, warp_stations, off);
+    if (lane == 0 && warp_stations) atomicAdd(a.out_station_total, warp_stations);
+  }
+}
+
+// Pass 1 of march.cu launch_split (full raster: pass 2 reads every pixel of
+// its own screen rectangle).  False when the probe does not apply.
+bool launch_iso_probe(const isc_render_args* a, cudaStream_t st, int* status) {
+  if (getenv("ISC_DISABLE_PAIRED_PROBE") || a->n_sources != 1 || !a->work_counter || a->ray_dirs ||
+      a->alpha_stop < 1.0 || !a->interpolation)
+    return false;
+  const isc_source& s = a->src[0];
+  if (s.mode != ISC_ISO || s.feature_dim != 1 || s.dtype != ISC_F32 || !s.has_guard) return false;
+  MultiField M;
+  if (!build_multi_field(a, M)) return false;
+  const bool contig = M.s[0].sx == 1;
+  const int tiles_x = (a->camera.width + 7) / 8, tiles_y = (a->camera.height + 1) / 2;
+  const int super_x = (tiles_x + 7) / 8, super_y = (tiles_y + 7) / 8;
+  const int n_codes = super_x * super_y * 64;
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (contig) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, iso_probe_kernel<true>, kThreads, 0);
+  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, iso_probe_kernel<false>, kThreads, 0);
+  int grid = sms * (per_sm > 0 ? per_sm : 1);
+  const int need = (n_codes + (kThreads / 32) - 1) / (kThreads / 32);
+  if (grid > need) grid = need > 0 ? need : 1;
+  if (contig)
+    iso_probe_kernel<true><<<grid, kThreads, 0, st>>>(*a, M, tiles_x, tiles_y, super_x, n_codes, 0, 0);
+  else
+    iso_probe_kernel<false><<<grid, kThreads, 0, st>>>(*a, M, tiles_x, tiles_y, super_x, n_codes, 0, 0);
+  const cudaError_t e = cudaGetLastError();
+  *status = e == cudaSuccess ? ISC_OK : cuda_fail(e, "iso_probe_kernel");
+  return true;
+}
+
+template <int NS, int DIMS, bool CONTIG>
 static int launch_multi_fast(const isc_render_args* a, const MultiField& M, cudaStream_t st) {
   static const int tw_log2 = getenv("ISC_MULTI_TILE_W") ? __builtin_ctz(atoi(getenv("ISC_MULTI_TILE_W"))) : 3;
   const int tw = 1 << tw_log2, th = 32 >> tw_log2;
@@ -742,11 +1010,12 @@ static int launch_multi_fast(const isc_render_args* a, const MultiField& M, cuda
   int dev = 0, sms = 148, per_sm = 1;
   ISC_CUDA_CHECK(cudaGetDevice(&dev));
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_multi_fast_kernel<NS, DIMS>, kMultiFastThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_multi_fast_kernel<NS, DIMS, CONTIG>,
+                                                kMultiFastThreads, 0);
   int grid = sms * (per_sm > 0 ? per_sm : 1);
   const int need = (n_codes + (kMultiFastThreads / 32) - 1) / (kMultiFastThreads / 32);
   if (grid > need) grid = need > 0 ? need : 1;
-  march_multi_fast_kernel<NS, DIMS><<<grid, kMultiFastThreads, 0, st>>>(*a, M, tiles_x, tiles_y, super_x, n_codes, tile_x0,
+  march_multi_fast_kernel<NS, DIMS, CONTIG><<<grid, kMultiFastThreads, 0, st>>>(*a, M, tiles_x, tiles_y, super_x, n_codes, tile_x0,
                                                                 tile_y0, tw_log2);
   ISC_CUDA_CHECK(cudaGetLastError());
   return ISC_OK;
@@ -757,13 +1026,25 @@ static bool launch_multi_fast_dims(const isc_render_args* a, const MultiField& M
   const int ns = a->n_sources;
   int dims = 0, scale = 1;
   for (int si = 0; si < ns; ++si, scale *= 5) dims += a->src[si].feature_dim * scale;
+  // C-contiguous (z, y, x[, c]) sources get the immediate-offset gather
+  bool contig = getenv("ISC_DISABLE_CONTIG") == nullptr;
+  for (int si = 0; si < ns; ++si)
+    contig &= M.s[si].sx == M.s[si].dim && (M.s[si].dim == 1 || M.s[si].sc == 1);
   switch (ns * 1000 + dims) {
-    case 1001: *status = launch_multi_fast<1, 1>(a, M, st); return true;
-    case 1003: *status = launch_multi_fast<1, 3>(a, M, st); return true;
-    case 2006: *status = launch_multi_fast<2, 1 + 5 * 1>(a, M, st); return true;
-    case 2016: *status = launch_multi_fast<2, 1 + 5 * 3>(a, M, st); return true;
-    case 2008: *status = launch_multi_fast<2, 3 + 5 * 1>(a, M, st); return true;
-    case 2018: *status = launch_multi_fast<2, 3 + 5 * 3>(a, M, st); return true;
+    case 1001: *status = contig ? launch_multi_fast<1, 1, true>(a, M, st) : launch_multi_fast<1, 1, false>(a, M, st); return true;
+    case 1003: *status = contig ? launch_multi_fast<1, 3, true>(a, M, st) : launch_multi_fast<1, 3, false>(a, M, st); return true;
+    case 2006:
+      *status = contig ? launch_multi_fast<2, 1 + 5 * 1, true>(a, M, st) : launch_multi_fast<2, 1 + 5 * 1, false>(a, M, st);
+      return true;
+    case 2016:
+      *status = contig ? launch_multi_fast<2, 1 + 5 * 3, true>(a, M, st) : launch_multi_fast<2, 1 + 5 * 3, false>(a, M, st);
+      return true;
+    case 2008:
+      *status = contig ? launch_multi_fast<2, 3 + 5 * 1, true>(a, M, st) : launch_multi_fast<2, 3 + 5 * 1, false>(a, M, st);
+      return true;
+    case 2018:
+      *status = contig ? launch_multi_fast<2, 3 + 5 * 3, true>(a, M, st) : launch_multi_fast<2, 3 + 5 * 3, false>(a, M, st);
+      return true;
     default: return false;
   }
 }

@@ -191,11 +191,12 @@ static __device__ __noinline__ void chain_step_rare(const isc_chain_step& st, fl
 template <int D>
 __device__ __forceinline__ float run_chain_fast(const isc_source& s, float v[4]) {
   bool reduced = (D == 1);
+  const unsigned ops = s.step_ops;
 #pragma unroll
   for (int i = 0; i < ISC_MAX_CHAIN; ++i) {
     if (i >= s.n_steps) break;
     const isc_chain_step& st = s.steps[i];
-    const int op = st.op;
+    const int op = (int)((ops >> (4 * i)) & 0xFu);
     if (op == ISC_OP_ADD) {
 #pragma unroll
       for (int c = 0; c < D; ++c) v[c] = fadd(v[c], st.arg[c]);

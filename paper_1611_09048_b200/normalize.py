@@ -44,6 +44,7 @@ def _source_struct(array, guard_arr: int, guard_dom: int, feature_dim: int, chai
         s.steps[j].op, s.steps[j].in_dim = op, in_dim
         s.steps[j].arg[:] = [float(v) for v in arg]
         s.steps[j].arg_d[:] = [float(v) for v in arg]
+        s.step_ops |= (op & 0xF) << (4 * j)
     return s
 
 

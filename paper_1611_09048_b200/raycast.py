@@ -214,6 +214,7 @@ def pack_render_args(domain, volume, scene: SceneState, plans: Sequence[SourcePl
             s.steps[j].in_dim = in_dim
             s.steps[j].arg[:] = [float(v) for v in arg]
             s.steps[j].arg_d[:] = [float(v) for v in arg]
+            s.step_ops |= (op & 0xF) << (4 * j)
     return a
 
 

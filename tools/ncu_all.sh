@@ -1,14 +1,19 @@
 #!/bin/bash
 # One `ncu --set full` capture of the dominant march kernel per bench config
-# (C1-C5 single camera, C4 3-point TF), summaries into profiles/$1/ and the
-# counters into profiles/ncu_counters.json.   usage: tools/ncu_all.sh r2
+# (C1-C5, single camera).  Writes the reports and the per-config summaries
+# under gpurun_out/ (the only directory gpurun brings back), and the
+# counters file gpurun_out/ncu_counters.json; copy the summaries to
+# profiles/$tag/ and the counters to profiles/ncu_counters.json afterwards
+# (tools/ncu_import.sh).   usage: tools/ncu_all.sh r2 [configs...]
 set -u
-tag=$1
-mkdir -p profiles/$tag gpurun_out
-for c in c4 c2 c3 c1 c5; do
-  ncu --set full --import-source on --clock-control none -k regex:march -c 1 -f -o gpurun_out/${tag}_$c \
+tag=$1; shift
+cfgs=${*:-c4 c2 c3 c1 c5}
+out=gpurun_out/ncu_$tag
+mkdir -p $out
+for c in $cfgs; do
+  ncu --set full --import-source on --clock-control none -k regex:march -c 1 -f -o $out/$c \
       python tools/time_march.py --config $c --reps 1 > /dev/null 2>&1
-  python tools/ncu_summary.py gpurun_out/${tag}_$c.ncu-rep > profiles/$tag/march_${c}_ncu.txt
-  python tools/ncu_lines.py gpurun_out/${tag}_$c.ncu-rep 30 >> profiles/$tag/march_${c}_ncu.txt
-  python tools/ncu_counters.py ${c}_n1 gpurun_out/${tag}_$c.ncu-rep profiles/$tag/march_${c}_ncu.txt
+  python tools/ncu_summary.py $out/$c.ncu-rep > $out/march_${c}_ncu.txt
+  python tools/ncu_lines.py $out/$c.ncu-rep 30 >> $out/march_${c}_ncu.txt
+  NCU_COUNTERS=$out/ncu_counters.json python tools/ncu_counters.py ${c}_n1 $out/$c.ncu-rep profiles/$tag/march_${c}_ncu.txt
 done

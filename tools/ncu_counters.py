@@ -14,7 +14,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-OUT = os.path.join(ROOT, "profiles", "ncu_counters.json")
+OUT = os.environ.get("NCU_COUNTERS") or os.path.join(ROOT, "profiles", "ncu_counters.json")
 METRICS = {
     "dram__bytes_read.sum": "dram_read_bytes",
     "dram__bytes_write.sum": "dram_write_bytes",

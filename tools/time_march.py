@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--alpha", type=float, default=None, help="early_termination_alpha (default: the config's 1.0)")
     ap.add_argument("--opacity", type=float, default=None, help="scale the transfer function's alpha ramp")
     ap.add_argument("--dtype", default="float32", help="field element type (float32, float16, bfloat16)")
+    ap.add_argument("--active", default=None, help="comma-separated source ids to render (C3: 0 = iso scalar, "
+                                                   "1 = float3 chain)")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
     n = cfg["n"]
@@ -46,6 +48,12 @@ def main():
         pts = {k: [(p[0], p[1], p[2], p[3], p[4] * args.opacity) for p in v] for k, v in scene.tf_points.items()}
         scene = P.SceneState(camera=scene.camera, tf_points=pts, value_ranges=scene.value_ranges,
                              chain_texts=scene.chain_texts, clip_planes=scene.clip_planes, settings=scene.settings)
+    if args.active is not None:
+        import dataclasses
+        ids = tuple(int(v) for v in args.active.split(","))
+        scene = P.SceneState(camera=scene.camera, tf_points=scene.tf_points, value_ranges=scene.value_ranges,
+                             chain_texts=scene.chain_texts, clip_planes=scene.clip_planes,
+                             settings=dataclasses.replace(scene.settings, active_set=ids))
     if args.alpha is not None:
         import dataclasses
         scene = P.SceneState(camera=scene.camera, tf_points=scene.tf_points, value_ranges=scene.value_ranges,
