@@ -959,9 +959,13 @@ __global__ void __launch_bounds__(kThreads, 4)
 }
 
 // Pass 1 of march.cu launch_split (full raster: pass 2 reads every pixel of
-// its own screen rectangle).  False when the probe does not apply.
+// its own screen rectangle).  Experiment switch ISC_PAIRED_PROBE=1: measured
+// slower than the multi-source kernel run on the iso source alone (C3 frame
+// 2.34 vs 2.14 ms; 64 registers with call-site spills around the iso pair
+// helpers, three shuffles per station pair), so the default probe is that
+// kernel.  False when the probe does not apply.
 bool launch_iso_probe(const isc_render_args* a, cudaStream_t st, int* status) {
-  if (getenv("ISC_DISABLE_PAIRED_PROBE") || a->n_sources != 1 || !a->work_counter || a->ray_dirs ||
+  if (!getenv("ISC_PAIRED_PROBE") || a->n_sources != 1 || !a->work_counter || a->ray_dirs ||
       a->alpha_stop < 1.0 || !a->interpolation)
     return false;
   const isc_source& s = a->src[0];
