@@ -357,6 +357,19 @@ def describe_kernel(plans: Sequence[SourcePlan], settings, analytic_lut: bool = 
                     line = 0
             return (f"isc::march_fast_kernel<INTERP={int(interp)},GUARDED={int(guarded)},PAIRED=1,"
                     f"LINE={line},DIM={dim},ET={int(et)},T={elem}>")
+    if (len(plans) == 2 and interp and not et and plans[0].mode == ISO_MODE and plans[1].mode != ISO_MODE
+            and plans[0].handle.descriptor.feature_dim == 1 and plans[1].handle.descriptor.feature_dim in (1, 3)
+            and all(p.handle.descriptor.has_guard for p in plans)
+            and all(getattr(p.handle.device_view(p.domain)[0], "dtype", None) in (_t.float32, np.float32)
+                    for p in plans)):
+        # split render (march.cu launch_split): iso probe, then the volume pass
+        pw = lut_analytic(plans[1].tf.lut) if analytic_lut else None
+        dim = plans[1].handle.descriptor.feature_dim
+        line = 1 + len(pw[2]) if pw is not None else 0
+        if line > _LINE_MAX.get(("float", dim, False), 1):
+            line = 0
+        return ("isc::march_multi_fast_kernel<NS=1,DIMS=[1]> (iso probe) + "
+                f"isc::march_fast_kernel<INTERP=1,GUARDED=1,PAIRED=1,LINE={line},DIM={dim},ET=0,T=float> (volume)")
     if 1 <= len(plans) <= 4:
         dims = [p.handle.descriptor.feature_dim for p in plans]
         if interp and all(p.handle.descriptor.has_guard for p in plans) and len(plans) <= 2 and \

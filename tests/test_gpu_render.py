@@ -751,3 +751,56 @@ def test_composite_user_functor_renders_like_its_expansion():
                              settings=P.RenderSettings(active_set=(0,), early_termination_alpha=1.0))
         imgs.append(P.render_local(ctx, scene).pixels)
     assert torch.equal(imgs[0], imgs[1]) and float(imgs[0][..., 3].max()) > 0
+
+
+@pytest.mark.parametrize("probe", ["default", "paired", "single-kernel"])
+def test_split_iso_volume_render_matches_oracle(probe, monkeypatch):
+    """Iso source + volume source scenes render in two passes (iso probe,
+    then the volume march stopped at each ray's hit, march.cu launch_split);
+    the paired probe (ISC_PAIRED_PROBE=1) and the single multi-source kernel
+    (ISC_DISABLE_SPLIT=1) give the same station counts and images within
+    float32 rounding, and all match the CPU oracle."""
+    import paper_1611_09048_b200 as P
+    from oracle import isaac_oracle as O
+    torch = _torch()
+    if probe == "paired":
+        monkeypatch.setenv("ISC_PAIRED_PROBE", "1")
+    if probe == "single-kernel":
+        monkeypatch.setenv("ISC_DISABLE_SPLIT", "1")
+    n = 28
+    rng = np.random.default_rng(41)
+    z, y, x = np.meshgrid(*(np.arange(-1, n + 1, dtype=np.float64),) * 3, indexing="ij")
+    scal = np.sqrt((x - n / 2) ** 2 + (y - n / 2 + 0.3) ** 2 + (z - n / 2 - 0.2) ** 2).astype(np.float32)
+    vec = rng.random((n + 2,) * 3 + (3,)).astype(np.float32)
+    cool = [(0.0, 0.0, 0.0, 0.0, 0.0), (0.6, 0.1, 0.7, 0.4, 0.3), (1.0, 0.7, 1.0, 0.9, 0.8)]
+    pos, look = (61.0, 47.0, -37.0), (14.0, 13.5, 14.5)
+    for decomp in ((1, 1, 1), (2, 1, 1)):
+        vol = P.GlobalVolume((n, n, n), decomp)
+        for rank in range(vol.rank_count):
+            dom = vol.local_domain(rank, 1)
+            (ox, oy, oz), (sx, sy, sz) = dom.offset, dom.size
+            sl = np.s_[oz:oz + sz + 2, oy:oy + sy + 2, ox:ox + sx + 2]
+            reg = P.SourceRegistry(dom)
+            reg.register_handle(P.array_backed_handle(P.SourceDescriptor("s", 1, has_guard=True),
+                                                      torch.from_numpy(np.ascontiguousarray(scal[sl])).cuda(), 1))
+            reg.register_handle(P.array_backed_handle(P.SourceDescriptor("v", 3, has_guard=True),
+                                                      torch.from_numpy(np.ascontiguousarray(vec[sl])).cuda(), 1))
+            P.update_sources(reg, {0, 1}, {})
+            fr = P.default_registry()
+            ctx = P.RankContext(vol, dom, reg, fr, fr.limits)
+            scene = P.SceneState(camera=P.Camera(pos, look, image_size=(72, 54)),
+                                 tf_points={0: [(0.0, 0.0, 0.0, 0.0, 0.0), (1.0, 1.0, 1.0, 1.0, 1.0)], 1: cool},
+                                 value_ranges={0: (0.0, 20.0), 1: (0.0, 6.0)},
+                                 chain_texts={0: "", 1: "length | mul(2) | add(0.1)"},
+                                 settings=P.RenderSettings(active_set=(0, 1), modes={0: "iso"},
+                                                           iso_thresholds={0: 9.5}, early_termination_alpha=1.0))
+            img = P.render_local(ctx, scene, keep_station_counts=True)
+            srcs = [O.Source(np.ascontiguousarray(scal[sl]), dom.offset, dom.size, 1,
+                             lut=O.lut_from_points(scene.tf_points[0]), value_range=(0.0, 20.0), mode="iso",
+                             iso_threshold=9.5),
+                    O.Source(np.ascontiguousarray(vec[sl]), dom.offset, dom.size, 1, lut=O.lut_from_points(cool),
+                             value_range=(0.0, 6.0), steps=O.parse_steps("length | mul(2) | add(0.1)", 3))]
+            ref = O.render_brick({"position": pos, "look_at": look, "width": 72, "height": 54},
+                                 O.Brick(dom.offset, dom.size, 1, (n, n, n), decomp), srcs)
+            assert np.abs(img.pixels.cpu().numpy() - ref.rgba).max() <= RGBA_TOL
+            assert np.array_equal(img.station_counts.cpu().numpy().astype(np.int64), ref.stations.reshape(-1))
