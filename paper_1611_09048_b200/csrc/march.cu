@@ -21,6 +21,8 @@
 
 #include "common.cuh"
 #include "launch_tuner.cuh"
+#include <mutex>
+
 #include "march_common.cuh"
 #include "raysetup.cuh"
 #include "sample.cuh"
@@ -29,6 +31,7 @@ namespace isc {
 
 bool launch_multi(const isc_render_args* a, cudaStream_t st, int* status);  // march_multi.cu
 bool launch_iso_probe(const isc_render_args* a, cudaStream_t st, int* status);  // march_multi.cu
+extern thread_local bool g_split_probe;                                           // march_multi.cu
 
 __device__ __forceinline__ void tile_pixel(int& px, int& py) {
   const int t = threadIdx.x, w = t >> 5, l = t & 31;
@@ -687,6 +690,22 @@ static int launch_split(const isc_render_args* a, cudaStream_t s, bool* handled)
   // scratch: shaded hits (float4), station counts (u32), the volume pass's tile counter
   char* scratch = nullptr;
   const size_t bytes = npx * (sizeof(float4) + sizeof(uint32_t)) + 16;
+  {  // keep the stream-ordered pool's memory between frames (default: returned to the OS at every sync)
+    static std::mutex mu;
+    static bool pool_kept[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    if (dev >= 0 && dev < 64 && !pool_kept[dev]) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+      cudaGetLastError();
+      pool_kept[dev] = true;
+    }
+  }
   ISC_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes, s));
   float4* shade = reinterpret_cast<float4*>(scratch);
   uint32_t* counts = a->out_stations ? a->out_stations : reinterpret_cast<uint32_t*>(scratch + npx * sizeof(float4));
@@ -697,8 +716,12 @@ static int launch_split(const isc_render_args* a, cudaStream_t s, bool* handled)
   iso.out_stations = counts;
   int status = ISC_OK;
   *handled = true;
+  // without caller-requested per-pixel outputs the probe may cull to the
+  // brick's screen rectangle: the volume pass reads only inside it
+  g_split_probe = a->out_stations == nullptr;
   if (!launch_iso_probe(&iso, s, &status) && !launch_multi(&iso, s, &status))
     status = fail(ISC_E_VALUE, "iso probe not launchable");
+  g_split_probe = false;
   if (status == ISC_OK) {
     // pass 2: the volume source, stopped at each ray's hit
     vol.out_stations = nullptr;

@@ -141,8 +141,12 @@ __device__ __forceinline__ void fast_gather(const FastField& F, const double p[3
 // False (no culling) when a corner is not strictly in front of the camera,
 // for explicit ray lists, and when per-pixel debug outputs are requested
 // (they are defined for every pixel).
-inline bool brick_screen_rect(const isc_render_args* a, int& x0, int& y0, int& x1, int& y1) {
-  if (a->ray_dirs || a->out_stations || a->out_hit || a->out_t || a->out_krange) return false;
+// stations_internal: out_stations is the split render's scratch (read back
+// only inside the same screen rectangle), so it does not force a full raster.
+inline bool brick_screen_rect(const isc_render_args* a, int& x0, int& y0, int& x1, int& y1,
+                              bool stations_internal = false) {
+  if (a->ray_dirs || (a->out_stations && !stations_internal) || a->out_hit || a->out_t || a->out_krange)
+    return false;
   const isc_camera& c = a->camera;
   double xmin = 1e300, xmax = -1e300, ymin = 1e300, ymax = -1e300;
   for (int corner = 0; corner < 8; ++corner) {

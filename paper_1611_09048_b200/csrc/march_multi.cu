@@ -993,6 +993,9 @@ bool launch_iso_probe(const isc_render_args* a, cudaStream_t st, int* status) {
   return true;
 }
 
+// Set by march.cu launch_split around its iso probe (same host thread).
+thread_local bool g_split_probe = false;
+
 template <int NS, int DIMS, bool CONTIG>
 static int launch_multi_fast(const isc_render_args* a, const MultiField& M, cudaStream_t st) {
   static const int tw_log2 = getenv("ISC_MULTI_TILE_W") ? __builtin_ctz(atoi(getenv("ISC_MULTI_TILE_W"))) : 3;
@@ -1001,7 +1004,7 @@ static int launch_multi_fast(const isc_render_args* a, const MultiField& M, cuda
   int tile_x0 = 0, tile_y0 = 0;
   int rx0, ry0, rx1, ry1;
   static const bool no_cull = getenv("ISC_DISABLE_CULL") != nullptr;
-  if (!no_cull && brick_screen_rect(a, rx0, ry0, rx1, ry1)) {  // see march.cu launch_fast
+  if (!no_cull && brick_screen_rect(a, rx0, ry0, rx1, ry1, g_split_probe)) {  // see march.cu launch_fast
     ISC_CUDA_CHECK(cudaMemsetAsync(a->out_rgba, 0, (size_t)a->camera.width * a->camera.height * sizeof(float4), st));
     tile_x0 = rx0 / tw;
     tile_y0 = ry0 / th;

@@ -23,4 +23,6 @@ for c in $cfgs; do
   else
     NCU_COUNTERS=$out/ncu_counters.json python tools/ncu_counters.py ${c}_n1 $out/$c.ncu-rep profiles/$tag/march_${c}_ncu.txt
   fi
+  # reports are large; gpurun brings back at most 64 MiB of gpurun_out/
+  if [ -z "${NCU_KEEP:-}" ]; then rm -f "gpurun_out/ncu_${tag}/${c}.ncu-rep"; fi
 done
