@@ -152,8 +152,8 @@ def test_c3_multi_source_iso_vs_oracle():
     got = img.pixels.reshape(-1, 4)[pix].cpu().numpy()
     err = np.abs(got - ref.rgba).max(axis=1)
     # an iso sign test in float32 vs float64 may flip on a pixel grazing the surface
-    assert (err > 1e-3).mean() <= 0.01, err.max()
-    assert (img.station_counts.cpu().numpy()[pix].astype(np.int64) != ref.stations).mean() <= 0.01
+    assert (err > 1e-3).sum() == 0, err.max()
+    assert (img.station_counts.cpu().numpy()[pix].astype(np.int64) != ref.stations).sum() == 0
 
 
 def _ctx_n(P, vol, rank, full):

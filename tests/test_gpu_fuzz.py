@@ -101,6 +101,6 @@ def test_random_scene_vs_oracle(seed):
         bad = np.abs(got - ref.rgba).max(axis=-1) > 1e-3
         st_bad = img.station_counts.cpu().numpy().reshape(c["h"], c["w"]).astype(np.int64) != \
             ref.stations.reshape(c["h"], c["w"])
-        allowed = max(2, int(0.004 * c["w"] * c["h"]))
+        allowed = 0
         assert bad.sum() <= allowed, (seed, r, c, np.abs(got - ref.rgba).max())
         assert st_bad.sum() <= allowed, (seed, r, c)
