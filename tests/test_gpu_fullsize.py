@@ -151,7 +151,7 @@ def test_c3_multi_source_iso_vs_oracle():
     ref = O.render_rays(cam.position, dirs, O.Brick((0, 0, 0), (n, n, n), 1, (n, n, n)), srcs)
     got = img.pixels.reshape(-1, 4)[pix].cpu().numpy()
     err = np.abs(got - ref.rgba).max(axis=1)
-    # an iso sign test in float32 vs float64 may flip on a pixel grazing the surface
+    # iso decisions are float64-exact (isc_source.iso_exact): no flipped pixel
     assert (err > 1e-3).sum() == 0, err.max()
     assert (img.station_counts.cpu().numpy()[pix].astype(np.int64) != ref.stations).sum() == 0
 
