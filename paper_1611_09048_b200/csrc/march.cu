@@ -263,8 +263,9 @@ __global__ void __launch_bounds__(kThreads) march_kernel(const __grid_constant__
 #endif
 // LINE: 0 = transfer function read from the shared-memory LUT, L >= 1 =
 // analytic piecewise-linear form with L-1 kinks (classify_line_premul<L>).
+// AOS3: float3 source in the standard interleaved layout (fast_gather_aos3).
 template <bool INTERP, bool GUARDED, bool PAIRED, int LINE = 0, int DIM = 1, bool ET = false,
-          typename T = float>
+          typename T = float, bool AOS3 = false>
 __global__ void __launch_bounds__(kThreads, ISC_FAST_MINB) march_fast_kernel(const __grid_constant__ isc_render_args a,
                                                               const FastField F, int tiles_x, int tiles_y,
                                                               int super_x, int n_codes, int row_order,
@@ -390,7 +391,8 @@ __global__ void __launch_bounds__(kThreads, ISC_FAST_MINB) march_fast_kernel(con
           } else {
             static_assert(INTERP && GUARDED && PAIRED, "vector sources: guarded trilinear paired path only");
             float vv[4] = {0.f, 0.f, 0.f, 0.f};
-            fast_gather<DIM, T>(F, p0, vv);
+            if constexpr (AOS3) fast_gather_aos3(F, p0, vv);
+            else fast_gather<DIM, T>(F, p0, vv);
             s0 = run_chain_fast<DIM>(s, vv);
           }
           if constexpr (LINE > 0) c = classify_line_premul<LINE>(s, lo, inv, s0);
@@ -588,7 +590,7 @@ static bool fast_eligible(const isc_render_args* a, FastField& F) {
 
 
 template <bool INTERP, bool GUARDED, bool PAIRED, int LINE = 0, int DIM = 1, bool ET = false,
-          typename T = float>
+          typename T = float, bool AOS3 = false>
 static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_t st) {
   static const int tw_env = getenv("ISC_TILE_W") ? __builtin_ctz(atoi(getenv("ISC_TILE_W"))) : -1;
   static const int cap_env = getenv("ISC_CTAS_PER_SM") ? atoi(getenv("ISC_CTAS_PER_SM")) : 0;
@@ -607,7 +609,7 @@ static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_
   OccupancyTuner::Choice ch{cap_env, tw_env >= 0 ? tw_env : 3};
   if (!cap_env && tw_env < 0 && !no_tune && PAIRED) {
     const int variant = (INTERP ? 1 : 0) | (GUARDED ? 2 : 0) | (ET ? 8 : 0) | (DIM << 4) | ((int)sizeof(T) << 8) |
-                        (LINE << 12);
+                        (LINE << 12) | (AOS3 ? 1 << 16 : 0);
     ch = tuner().choose(OccupancyTuner::make_key(a, variant), st, &ev0, &ev1);
   }
   const int tw_log2 = ch.tw_log2;
@@ -626,14 +628,15 @@ static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_
   int dev = 0, sms = 148, per_sm = 1;
   ISC_CUDA_CHECK(cudaGetDevice(&dev));
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_fast_kernel<INTERP, GUARDED, PAIRED, LINE, DIM, ET, T>,
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm,
+                                                march_fast_kernel<INTERP, GUARDED, PAIRED, LINE, DIM, ET, T, AOS3>,
                                                 kThreads, 0);
   if (ch.cap > 0 && per_sm > ch.cap) per_sm = ch.cap;
   int grid = sms * (per_sm > 0 ? per_sm : 1);
   const int need = (n_codes + (kThreads / 32) - 1) / (kThreads / 32);  // one tile per warp at most
   if (grid > need) grid = need > 0 ? need : 1;
   if (ev0) cudaEventRecord(ev0, st);
-  march_fast_kernel<INTERP, GUARDED, PAIRED, LINE, DIM, ET, T><<<grid, kThreads, 0, st>>>(
+  march_fast_kernel<INTERP, GUARDED, PAIRED, LINE, DIM, ET, T, AOS3><<<grid, kThreads, 0, st>>>(
       *a, F, tiles_x, tiles_y, super_x, n_codes, row_order ? 1 : 0, tw_log2, tile_x0, tile_y0);
   ISC_CUDA_CHECK(cudaGetLastError());
   if (ev1) cudaEventRecord(ev1, st);
@@ -647,17 +650,31 @@ int launch_staged(int lines, const isc_render_args* a, const FastField& F, cudaS
 // Guarded trilinear paired march with the analytic transfer function of
 // `lines` pieces when this instantiation covers it (lines <= MAXL), else the
 // shared-memory LUT.  MAXL bounds the template instantiations per variant.
-template <int MAXL, int DIM, bool ET, typename T>
+template <int MAXL, int DIM, bool ET, typename T, bool AOS3 = false>
 static int launch_line(int lines, const isc_render_args* a, const FastField& F, cudaStream_t st) {
   if (lines > MAXL) lines = 0;
   switch (lines) {
-    case 1: return launch_fast<true, true, true, 1, DIM, ET, T>(a, F, st);
-    case 2: if constexpr (MAXL >= 2) return launch_fast<true, true, true, 2, DIM, ET, T>(a, F, st); break;
-    case 3: if constexpr (MAXL >= 3) return launch_fast<true, true, true, 3, DIM, ET, T>(a, F, st); break;
-    case 4: if constexpr (MAXL >= 4) return launch_fast<true, true, true, 4, DIM, ET, T>(a, F, st); break;
+    case 1: return launch_fast<true, true, true, 1, DIM, ET, T, AOS3>(a, F, st);
+    case 2: if constexpr (MAXL >= 2) return launch_fast<true, true, true, 2, DIM, ET, T, AOS3>(a, F, st); break;
+    case 3: if constexpr (MAXL >= 3) return launch_fast<true, true, true, 3, DIM, ET, T, AOS3>(a, F, st); break;
+    case 4: if constexpr (MAXL >= 4) return launch_fast<true, true, true, 4, DIM, ET, T, AOS3>(a, F, st); break;
     default: break;
   }
-  return launch_fast<true, true, true, 0, DIM, ET, T>(a, F, st);
+  return launch_fast<true, true, true, 0, DIM, ET, T, AOS3>(a, F, st);
+}
+
+// float3 source in the standard interleaved layout with even row / slice
+// strides and an 8-byte aligned base (fast_gather_aos3).
+static bool aos3_layout(const FastField& F) {
+  static const bool off = getenv("ISC_DISABLE_AOS3") != nullptr;
+  return !off && F.sx == 3 && F.sc == 1 && F.sy % 2 == 0 && F.sz % 2 == 0 &&
+         reinterpret_cast<uintptr_t>(F.f) % 8 == 0;
+}
+
+template <int MAXL, bool ET>
+static int launch_line3(int lines, const isc_render_args* a, const FastField& F, cudaStream_t st) {
+  return aos3_layout(F) ? launch_line<MAXL, 3, ET, float, true>(lines, a, F, st)
+                        : launch_line<MAXL, 3, ET, float>(lines, a, F, st);
 }
 
 // C3-style scenes -- one scalar iso source followed by one volume source,
@@ -736,7 +753,7 @@ static int launch_split(const isc_render_args* a, cudaStream_t s, bool* handled)
     if (e != cudaSuccess) status = cuda_fail(e, "cudaMemsetAsync");
     const int lines = vol.src[0].lut_linear != 0 ? 1 + vol.src[0].lut_kinks : 0;
     if (status == ISC_OK)
-      status = vol.src[0].feature_dim == 3 ? launch_line<2, 3, false, float>(lines, &vol, F, s)
+      status = vol.src[0].feature_dim == 3 ? launch_line3<2, false>(lines, &vol, F, s)
                                            : launch_line<4, 1, false, float>(lines, &vol, F, s);
   }
   const cudaError_t e = cudaFreeAsync(scratch, s);
@@ -770,7 +787,7 @@ extern "C" int isc_render_local(const isc_render_args* a, void* stream) {
                 : launch_line<1, 1, false, __nv_bfloat16>(lines, a, F, s);
     }
     if (a->src[0].feature_dim == 3)
-      return et ? launch_line<2, 3, true, float>(lines, a, F, s) : launch_line<2, 3, false, float>(lines, a, F, s);
+      return et ? launch_line3<2, true>(lines, a, F, s) : launch_line3<2, false>(lines, a, F, s);
     // early termination, guarded trilinear: paired with the per-station stop test
     if (interp && guarded && !no_pair && et) return launch_line<4, 1, true, float>(lines, a, F, s);
     const bool stage = getenv("ISC_STAGE") != nullptr;  // shared-memory brick staging (march_staged.cu), read per call

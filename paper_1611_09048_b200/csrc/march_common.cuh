@@ -134,6 +134,45 @@ __device__ __forceinline__ void fast_gather(const FastField& F, const double p[3
   }
 }
 
+// fast_gather<3> for the standard AoS float3 layout (x contiguous,
+// components interleaved: sx == 3, sc == 1, even row / slice strides, an
+// 8-byte aligned base): the 6 floats of a corner row (x0 and x0 + 1, three
+// components each) come from 3 aligned 8-byte loads when x0 is even, and
+// from the 8-byte words around them (+ one 4-byte load of the last float)
+// when x0 is odd -- 16 load requests per station instead of 24 (each request
+// touches the same cache lines either way).  Same arithmetic as fast_gather.
+__device__ __forceinline__ void fast_gather_aos3(const FastField& F, const double p[3], float v[4]) {
+  const float* __restrict__ fld = reinterpret_cast<const float*>(F.f);
+  int ix, iy, iz;
+  const double flx = floor_split(p[0], ix), fly = floor_split(p[1], iy), flz = floor_split(p[2], iz);
+  const float fx = (float)dsub(p[0], flx), fy = (float)dsub(p[1], fly), fz = (float)dsub(p[2], flz);
+  const int x0 = ix - F.lo[0], y0 = iy - F.lo[1], z0 = iz - F.lo[2];
+  const bool odd = (x0 & 1) != 0;  // parity of the element offset (even strides)
+  const float* r00 = fld + ((z0 * F.sz + y0 * F.sy + 3 * x0) & ~1);
+  const float* rows[4] = {r00, r00 + F.sy, r00 + F.sz, r00 + F.sz + F.sy};
+  float c[4][6];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const float2* q = reinterpret_cast<const float2*>(rows[r]);
+    const float2 w0 = __ldg(q), w1 = __ldg(q + 1), w2 = __ldg(q + 2);
+    float t = 0.f;
+    if (odd) t = __ldg(rows[r] + 6);
+    c[r][0] = odd ? w0.y : w0.x;
+    c[r][1] = odd ? w1.x : w0.y;
+    c[r][2] = odd ? w1.y : w1.x;
+    c[r][3] = odd ? w2.x : w1.y;
+    c[r][4] = odd ? w2.y : w2.x;
+    c[r][5] = odd ? t : w2.y;
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const float a0 = fmaf(fx, c[0][3 + k] - c[0][k], c[0][k]), a1 = fmaf(fx, c[1][3 + k] - c[1][k], c[1][k]);
+    const float a2 = fmaf(fx, c[2][3 + k] - c[2][k], c[2][k]), a3 = fmaf(fx, c[3][3 + k] - c[3][k], c[3][k]);
+    const float b0 = fmaf(fy, a1 - a0, a0), b1 = fmaf(fy, a3 - a2, a2);
+    v[k] = fmaf(fz, b1 - b0, b0);
+  }
+}
+
 // Host: conservative pixel rectangle [x0, x1) x [y0, y1) outside which no
 // primary ray can hit the brick -- the bounding box of the pinhole projection
 // of the brick's 8 corners (the image of a box in front of the camera is the

@@ -777,17 +777,27 @@ static bool build_multi_field(const isc_render_args* a, MultiField& M);
 // Paired iso probe: pass 1 of the split iso + volume render (march.cu
 // launch_split).  ONE guarded float32 scalar iso source, no early
 // termination.  A warp is 16 rays (8x2 pixels) x 2 station parities as in
-// march_fast_kernel: the even lane tests the pair (k-1, k) for k = k_lo + 2j,
-// the odd lane the pair (k, k+1); the earlier station's value reaches the
-// later lane by a shuffle, in float64 (the multi-source kernel's exact iso
-// decisions: identity chains take the float64 value inside the error band,
-// add / mul chains always).  The ray's first hit in station order ends it
-// (at one station a backward pair wins over the forward exit pair, as in
-// _iso_detect); after the loop the even lane shades the hit (gradient
-// normal, raycast.py:210-242, 351-369) and writes the shaded colour to
-// out_rgba and the stations marched (hit station included) to out_stations.
-template <bool CONTIG>
-__global__ void __launch_bounds__(kThreads, 4)
+// march_fast_kernel: lane q marches the even stations k_lo + 2j of ray q,
+// lane q + 16 the odd ones, so one gather request covers 32 samples within an
+// 8x2-pixel footprint.  Station values are float64 (the multi-source kernel's
+// exact iso decisions: identity chains take the float64 value inside the
+// float32 error band, add / mul chains always).  Per iteration each lane
+// tests the backward pair ending at its own station (_iso_detect,
+// raycast.py:384-468): the odd lane's earlier value comes from the even lane
+// by one shuffle-up, the even lane's from the odd lane of the previous
+// iteration by one shuffle-down; one ballot tells both lanes of a pair
+// whether the ray hit (the even lane's station comes first).  The loop holds
+// no calls: the entry pair's value (station k_lo - 1 through the guard) is
+// sampled before it, the forward exit pair (tested only when no backward
+// pair hit) after it, and the hit is shaded after it by the lane that found
+// it (gradient normal, raycast.py:210-242, 351-369).  Outputs: the shaded hit
+// colour (alpha 1) or 0 in out_rgba, the stations marched (hit station
+// included) in out_stations -- what pass 2 stops at.
+#ifndef ISC_PROBE_MINB
+#define ISC_PROBE_MINB 4
+#endif
+template <bool CONTIG, bool CHAIN>
+__global__ void __launch_bounds__(kThreads, ISC_PROBE_MINB)
     iso_probe_kernel(const __grid_constant__ isc_render_args a, const __grid_constant__ MultiField M, int tiles_x,
                      int tiles_y, int super_x, int n_codes, int tile_x0, int tile_y0) {
   const int lane = threadIdx.x & 31, q = lane & 15, parity = lane >> 4;
@@ -827,8 +837,8 @@ __global__ void __launch_bounds__(kThreads, 4)
         reinterpret_cast<int4*>(a.out_krange)[pix] =
             make_int4((int)r.k_lo, (int)r.k_hi, (int)r.kg_lo, (int)r.kg_hi);
     }
-    const int k_lo = (int)r.k_lo, k_hi = (int)r.k_hi, kg_lo = (int)r.kg_lo, kg_hi = (int)r.kg_hi;
-    // guard contract per ray (march_multi_fast_kernel): stations up to kend
+    const int k_lo = (int)r.k_lo, k_hi = (int)r.k_hi;
+    // guard contract per ray (march_multi_fast_kernel): stations below kend
     int kend = k_hi;
     bool bad_tail = false;
     if (r.hit && k_hi > k_lo) {
@@ -852,19 +862,20 @@ __global__ void __launch_bounds__(kThreads, 4)
       }
     }
     const int n = r.hit ? max(kend - k_lo, 0) : 0;
+    // even lane: value at its station's predecessor (the entry pair through the guard first)
+    double prev = (double)CUDART_NAN_F;
+    if (!parity && n > 0 && k_lo - 1 >= (int)r.kg_lo) prev = iso_entry_value(a, M, 0, r.d[0], r.d[1], r.d[2], k_lo, err);
     const unsigned trips = __reduce_max_sync(0xffffffffu, (unsigned)((n + 1) >> 1));
-    double prev_even = (double)CUDART_NAN_F;   // even lane: value at k - 1
-    int hit_k = -1;
-    double hit_tau = 0.0, hit_cur = 0.0;
-    bool hit_back = false, done = false;
-    uint32_t stations = 0;
-    int kk = k_lo + parity;
-    for (unsigned j = 0; j < trips; ++j, kk += 2) {
-      const bool valid = !done && kk < kend;
+    double kd = (double)(k_lo + parity);
+    int left = n - parity;          // this lane's remaining stations
+    bool hit = false, done = false; // done: the ray (both lanes) hit
+    double hit_kd = 0.0, hit_sa = 0.0, hit_sb = 0.0, last = (double)CUDART_NAN_F;
+    for (unsigned j = 0; j < trips; ++j, left -= 2, kd = dadd(kd, 2.0)) {
+      const bool valid = left > 0 && !done;
       double cur = (double)CUDART_NAN_F;
-      double p[3] = {0.0, 0.0, 0.0};
       if (valid) {
-        station_pos(o, r.d, dmul((double)kk, step), p);
+        double p[3];
+        station_pos(o, r.d, dmul(kd, step), p);
         int ix, iy, iz;
         double fxd, fyd, fzd;
         cell_of_d(p, ix, iy, iz, fxd, fyd, fzd);
@@ -872,81 +883,75 @@ __global__ void __launch_bounds__(kThreads, 4)
         float c[8];
         if constexpr (CONTIG) corners_contig(S, x0, y0, z0, c);
         else corners_guarded(S, x0, y0, z0, c);
-        float v[4] = {lerp8(c, (float)fxd, (float)fyd, (float)fzd), 0.f, 0.f, 0.f};
-        cur = (double)run_chain_fast<1>(s, v);
-        if (s.iso_exact) {
-          if (s.n_steps == 0) {  // the error band of march_multi_fast_kernel
-            float m = fabsf(c[0]);
+        if constexpr (!CHAIN) {  // identity chain: float64 only inside the float32 error band
+          cur = (double)lerp8(c, (float)fxd, (float)fyd, (float)fzd);
+          float m = fabsf(c[0]);
 #pragma unroll
-            for (int i = 1; i < 8; ++i) m = fmaxf(m, fabsf(c[i]));
-            if (!(fabs(dsub(cur, thr)) > (double)m * 0x1p-18)) cur = trilinear_d(c, fxd, fyd, fzd);
-          } else {
-            cur = run_chain_d(s, trilinear_d(c, fxd, fyd, fzd));
-          }
+          for (int i = 1; i < 8; ++i) m = fmaxf(m, fabsf(c[i]));
+          if (!(fabs(dsub(cur, thr)) > (double)m * 0x1p-18)) cur = trilinear_d(c, fxd, fyd, fzd);
+        } else if (s.iso_exact) {  // add / mul chain: always the reference's float64
+          cur = run_chain_d(s, trilinear_d(c, fxd, fyd, fzd));
+        } else {
+          float v[4] = {lerp8(c, (float)fxd, (float)fyd, (float)fzd), 0.f, 0.f, 0.f};
+          cur = (double)run_chain_fast<1>(s, v);
         }
+        last = cur;
       }
       const double from_even = __shfl_up_sync(0xffffffffu, cur, 16);
-      double prev = parity ? from_even : prev_even;
-      if (!parity && valid && kk == k_lo && k_lo - 1 >= kg_lo)  // entry pair through the guard
-        prev = iso_entry_value(a, M, 0, r.d[0], r.d[1], r.d[2], kk, err);
-      // backward pair: keep s_prev (tau's numerator, computed after the loop
-      // from prev and the station's own value); forward exit pair: tau now
-      bool hit = false;
-      double tau = 0.0;   // backward: s_prev; forward: the crossing fraction
-      bool back = false;
-      if (valid) {
-        const double sa = dsub(prev, thr), sb = dsub(cur, thr);
-        hit = isfinite(sa) && ((sa < 0.0) != (sb < 0.0));
-        if (hit) {
-          tau = sa;
-          back = true;
-        } else if (kk == k_hi - 1 && kk + 1 < kg_hi) {  // exit pair, checked forward
-          double tx = 0.0;
-          if (iso_exit_pair(a, M, 0, r.d[0], r.d[1], r.d[2], kk, p[0], p[1], p[2], sb, &tx, err)) {
-            hit = true;
-            tau = tx;
-          }
-        }
+      const double before = parity ? from_even : prev;
+      const double sa = dsub(before, thr), sb = dsub(cur, thr);
+      const bool h = valid && isfinite(sa) && ((sa < 0.0) != (sb < 0.0));
+      const unsigned hits = __ballot_sync(0xffffffffu, h);
+      const bool even_hit = (hits >> q) & 1u, pair_hit = ((hits >> q) | (hits >> (q + 16))) & 1u;
+      if (h && !(parity && even_hit)) {  // the ray's first hit in station order
+        hit = true;
+        hit_kd = kd;
+        hit_sa = sa;
+        hit_sb = sb;
       }
-      // the even lane takes the odd lane's verdict: its station follows
-      const int odd_bits = __shfl_down_sync(0xffffffffu, (valid ? 1 : 0) | (hit ? 2 : 0) | (back ? 4 : 0), 16);
-      const double odd_tau = __shfl_down_sync(0xffffffffu, tau, 16);
-      const double odd_cur = __shfl_down_sync(0xffffffffu, cur, 16);
-      if (!parity && valid) {
-        ++stations;
-        if (hit) {
-          hit_k = kk;
-          hit_tau = tau;
-          hit_back = back;
-          hit_cur = cur;
-          done = true;
-        } else if (odd_bits & 1) {
-          ++stations;
-          if (odd_bits & 2) {
-            hit_k = kk + 1;
-            hit_tau = odd_tau;
-            hit_back = (odd_bits & 4) != 0;
-            hit_cur = odd_cur;
-            done = true;
-          }
-        }
-      }
-      prev_even = odd_cur;
-      done = __shfl_sync(0xffffffffu, done, q) != 0;  // the odd lane follows its pair
-      if (__all_sync(0xffffffffu, done || kk + 2 >= kend)) break;
+      done = done || pair_hit;
+      prev = __shfl_down_sync(0xffffffffu, cur, 16);  // even lane: the odd station before its next one
+      if (__all_sync(0xffffffffu, done || left <= 2)) break;
     }
-    if (parity || !in_img) continue;
-    if (bad_tail && hit_k < 0 && err) atomicAdd(err, 1u);  // marched into the bad tail
+    // Forward exit pair (k_hi - 1, k_hi) when no backward pair hit: the
+    // last station's value sits in the even lane when n is odd, else in the
+    // odd lane (raycast.py:384-468; the next brick cannot reach back).
+    const double odd_last = __shfl_down_sync(0xffffffffu, last, 16);
+    double hit_tau = 0.0;
+    bool hit_back = true;
+    if (!parity && !done && n > 0 && kend == k_hi && k_hi < (int)r.kg_hi) {
+      const int kl = k_hi - 1;
+      const double sb = dsub((n & 1) ? last : odd_last, thr);
+      double pl[3];
+      station_pos(o, r.d, dmul((double)kl, step), pl);
+      if (iso_exit_pair(a, M, 0, r.d[0], r.d[1], r.d[2], kl, pl[0], pl[1], pl[2], sb, &hit_tau, err)) {
+        hit = true;
+        hit_back = false;
+        hit_kd = (double)kl;
+      }
+    }
     float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (hit_k >= 0) {
+    if (hit) {  // both lanes of the warp that hold a hit shade together
       if (hit_back) {  // tau = s_prev / (s_prev - s_cur), raycast.py:434-437
-        const double den = dsub(hit_tau, dsub(hit_cur, thr));
-        hit_tau = den != 0.0 ? ddiv(hit_tau, den) : 1.0;
+        const double den = dsub(hit_sa, hit_sb);
+        hit_tau = den != 0.0 ? ddiv(hit_sa, den) : 1.0;
       }
       double ph[3];
-      station_pos(o, r.d, dmul((double)hit_k, step), ph);
+      station_pos(o, r.d, dmul(hit_kd, step), ph);
       c = iso_hit_color(a, M, 0, r.d[0], r.d[1], r.d[2], ph[0], ph[1], ph[2], hit_tau, hit_back ? -1.0 : 0.0, err);
     }
+    // the even lane writes the pixel: its own hit, else the odd lane's
+    const float4 co = shfl_down16(c);
+    const double kd_odd = __shfl_down_sync(0xffffffffu, hit_kd, 16);
+    const bool odd_hit = __shfl_down_sync(0xffffffffu, hit ? 1 : 0, 16) != 0;
+    if (parity || !in_img) continue;
+    if (!hit && odd_hit) {
+      c = co;
+      hit_kd = kd_odd;
+      hit = true;
+    }
+    if (bad_tail && !hit && err) atomicAdd(err, 1u);  // marched into the bad tail
+    const uint32_t stations = hit ? (uint32_t)((int)hit_kd - k_lo + 1) : (uint32_t)n;
     reinterpret_cast<float4*>(a.out_rgba)[pix] = c;
     if (a.out_stations) a.out_stations[pix] = stations;
     warp_stations += stations;
@@ -958,38 +963,53 @@ __global__ void __launch_bounds__(kThreads, 4)
   }
 }
 
-// Pass 1 of march.cu launch_split (full raster: pass 2 reads every pixel of
-// its own screen rectangle).  Experiment switch ISC_PAIRED_PROBE=1: measured
-// slower than the multi-source kernel run on the iso source alone (C3 frame
-// 2.34 vs 2.14 ms; 64 registers with call-site spills around the iso pair
-// helpers, three shuffles per station pair), so the default probe is that
-// kernel.  False when the probe does not apply.
+// Pass 1 of march.cu launch_split.  Culls to the brick's screen rectangle
+// when the caller asked for no per-pixel outputs (pass 2 reads the scratch
+// only inside the same rectangle; the shaded-hit scratch is cleared first,
+// pass 2 composites it behind every pixel it writes).  False when the probe
+// does not apply; ISC_DISABLE_PAIRED_PROBE=1 routes the probe to the
+// multi-source kernel (the round-2 default, A/B).
+extern thread_local bool g_split_probe;
 bool launch_iso_probe(const isc_render_args* a, cudaStream_t st, int* status) {
-  if (!getenv("ISC_PAIRED_PROBE") || a->n_sources != 1 || !a->work_counter || a->ray_dirs ||
-      a->alpha_stop < 1.0 || !a->interpolation)
+  static const bool off = getenv("ISC_DISABLE_PAIRED_PROBE") != nullptr;
+  if (off || a->n_sources != 1 || !a->work_counter || a->ray_dirs || a->alpha_stop < 1.0 || !a->interpolation)
     return false;
   const isc_source& s = a->src[0];
   if (s.mode != ISC_ISO || s.feature_dim != 1 || s.dtype != ISC_F32 || !s.has_guard) return false;
   MultiField M;
   if (!build_multi_field(a, M)) return false;
   const bool contig = M.s[0].sx == 1;
-  const int tiles_x = (a->camera.width + 7) / 8, tiles_y = (a->camera.height + 1) / 2;
+  int tiles_x = (a->camera.width + 7) / 8, tiles_y = (a->camera.height + 1) / 2;
+  int tile_x0 = 0, tile_y0 = 0;
+  int rx0, ry0, rx1, ry1;
+  static const bool no_cull = getenv("ISC_DISABLE_CULL") != nullptr;
+  *status = ISC_OK;
+  if (!no_cull && brick_screen_rect(a, rx0, ry0, rx1, ry1, g_split_probe)) {
+    const cudaError_t e = cudaMemsetAsync(a->out_rgba, 0, (size_t)a->camera.width * a->camera.height * sizeof(float4), st);
+    if (e != cudaSuccess) {
+      *status = cuda_fail(e, "cudaMemsetAsync");
+      return true;
+    }
+    tile_x0 = rx0 / 8;
+    tile_y0 = ry0 / 2;
+    tiles_x = rx1 > rx0 ? (rx1 + 7) / 8 - tile_x0 : 0;
+    tiles_y = ry1 > ry0 ? (ry1 + 1) / 2 - tile_y0 : 0;
+    if (tiles_x == 0 || tiles_y == 0) return true;
+  }
   const int super_x = (tiles_x + 7) / 8, super_y = (tiles_y + 7) / 8;
   const int n_codes = super_x * super_y * 64;
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (contig) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, iso_probe_kernel<true>, kThreads, 0);
-  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, iso_probe_kernel<false>, kThreads, 0);
+  auto kern = contig ? (s.n_steps ? iso_probe_kernel<true, true> : iso_probe_kernel<true, false>)
+                     : (s.n_steps ? iso_probe_kernel<false, true> : iso_probe_kernel<false, false>);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0);
   int grid = sms * (per_sm > 0 ? per_sm : 1);
   const int need = (n_codes + (kThreads / 32) - 1) / (kThreads / 32);
   if (grid > need) grid = need > 0 ? need : 1;
-  if (contig)
-    iso_probe_kernel<true><<<grid, kThreads, 0, st>>>(*a, M, tiles_x, tiles_y, super_x, n_codes, 0, 0);
-  else
-    iso_probe_kernel<false><<<grid, kThreads, 0, st>>>(*a, M, tiles_x, tiles_y, super_x, n_codes, 0, 0);
+  kern<<<grid, kThreads, 0, st>>>(*a, M, tiles_x, tiles_y, super_x, n_codes, tile_x0, tile_y0);
   const cudaError_t e = cudaGetLastError();
-  *status = e == cudaSuccess ? ISC_OK : cuda_fail(e, "iso_probe_kernel");
+  if (e != cudaSuccess) *status = cuda_fail(e, "iso_probe_kernel");
   return true;
 }
 

@@ -368,7 +368,8 @@ def describe_kernel(plans: Sequence[SourcePlan], settings, analytic_lut: bool = 
         line = 1 + len(pw[2]) if pw is not None else 0
         if line > _LINE_MAX.get(("float", dim, False), 1):
             line = 0
-        return ("isc::march_multi_fast_kernel<NS=1,DIMS=[1]> (iso probe) + "
+        chain = "1" if plans[0].chain.steps else "0"
+        return (f"isc::iso_probe_kernel<CHAIN={chain}> (paired iso probe) + "
                 f"isc::march_fast_kernel<INTERP=1,GUARDED=1,PAIRED=1,LINE={line},DIM={dim},ET=0,T=float> (volume)")
     if 1 <= len(plans) <= 4:
         dims = [p.handle.descriptor.feature_dim for p in plans]

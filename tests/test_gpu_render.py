@@ -749,18 +749,22 @@ def test_composite_user_functor_renders_like_its_expansion():
     assert torch.equal(imgs[0], imgs[1]) and float(imgs[0][..., 3].max()) > 0
 
 
-@pytest.mark.parametrize("probe", ["default", "paired", "single-kernel"])
-def test_split_iso_volume_render_matches_oracle(probe, monkeypatch):
+@pytest.mark.parametrize("iso_chain", ["", "mul(1.5) | add(-4.75)", "pow(2) | mul(0.1)"])
+@pytest.mark.parametrize("probe", ["paired", "multi-probe", "single-kernel"])
+def test_split_iso_volume_render_matches_oracle(probe, iso_chain, monkeypatch):
     """Iso source + volume source scenes render in two passes (iso probe,
     then the volume march stopped at each ray's hit, march.cu launch_split);
-    the paired probe (ISC_PAIRED_PROBE=1) and the single multi-source kernel
+    the paired probe (default), the multi-source kernel as the probe
+    (ISC_DISABLE_PAIRED_PROBE=1) and the single multi-source kernel
     (ISC_DISABLE_SPLIT=1) give the same station counts and images within
-    float32 rounding, and all match the CPU oracle."""
+    float32 rounding, and all match the CPU oracle -- for an identity iso
+    chain, an add / mul chain (float64 decisions) and a general chain; the
+    culled render (no per-pixel outputs) equals the full-raster one."""
     import paper_1611_09048_b200 as P
     from oracle import isaac_oracle as O
     torch = _torch()
-    if probe == "paired":
-        monkeypatch.setenv("ISC_PAIRED_PROBE", "1")
+    if probe == "multi-probe":
+        monkeypatch.setenv("ISC_DISABLE_PAIRED_PROBE", "1")
     if probe == "single-kernel":
         monkeypatch.setenv("ISC_DISABLE_SPLIT", "1")
     n = 28
@@ -787,13 +791,15 @@ def test_split_iso_volume_render_matches_oracle(probe, monkeypatch):
             scene = P.SceneState(camera=P.Camera(pos, look, image_size=(72, 54)),
                                  tf_points={0: [(0.0, 0.0, 0.0, 0.0, 0.0), (1.0, 1.0, 1.0, 1.0, 1.0)], 1: cool},
                                  value_ranges={0: (0.0, 20.0), 1: (0.0, 6.0)},
-                                 chain_texts={0: "", 1: "length | mul(2) | add(0.1)"},
+                                 chain_texts={0: iso_chain, 1: "length | mul(2) | add(0.1)"},
                                  settings=P.RenderSettings(active_set=(0, 1), modes={0: "iso"},
                                                            iso_thresholds={0: 9.5}, early_termination_alpha=1.0))
             img = P.render_local(ctx, scene, keep_station_counts=True)
+            culled = P.render_local(ctx, scene)
+            assert torch.equal(culled.pixels, img.pixels)
             srcs = [O.Source(np.ascontiguousarray(scal[sl]), dom.offset, dom.size, 1,
                              lut=O.lut_from_points(scene.tf_points[0]), value_range=(0.0, 20.0), mode="iso",
-                             iso_threshold=9.5),
+                             iso_threshold=9.5, steps=O.parse_steps(iso_chain, 1)),
                     O.Source(np.ascontiguousarray(vec[sl]), dom.offset, dom.size, 1, lut=O.lut_from_points(cool),
                              value_range=(0.0, 6.0), steps=O.parse_steps("length | mul(2) | add(0.1)", 3))]
             ref = O.render_brick({"position": pos, "look_at": look, "width": 72, "height": 54},

@@ -13,13 +13,13 @@ mkdir -p $out
 for c in $cfgs; do
   # C3 renders in two passes (iso probe + volume march): capture both
   n=1; [ "$c" = c3 ] && n=2
-  ncu --set full --import-source on --clock-control none -k regex:march -c $n -f -o $out/$c \
+  ncu --set full --import-source on --clock-control none -k regex:"march|iso_probe" -c $n -f -o $out/$c \
       python tools/time_march.py --config $c --reps 1 > /dev/null 2>&1
   python tools/ncu_summary.py $out/$c.ncu-rep > $out/march_${c}_ncu.txt
   python tools/ncu_lines.py $out/$c.ncu-rep 30 >> $out/march_${c}_ncu.txt
   if [ "$c" = c3 ]; then
     NCU_COUNTERS=$out/ncu_counters.json python tools/ncu_counters.py c3_n1 $out/$c.ncu-rep profiles/$tag/march_c3_ncu.txt march_fast_kernel
-    NCU_COUNTERS=$out/ncu_counters.json python tools/ncu_counters.py c3_probe_n1 $out/$c.ncu-rep profiles/$tag/march_c3_ncu.txt march_multi_fast
+    NCU_COUNTERS=$out/ncu_counters.json python tools/ncu_counters.py c3_probe_n1 $out/$c.ncu-rep profiles/$tag/march_c3_ncu.txt iso_probe
   else
     NCU_COUNTERS=$out/ncu_counters.json python tools/ncu_counters.py ${c}_n1 $out/$c.ncu-rep profiles/$tag/march_${c}_ncu.txt
   fi

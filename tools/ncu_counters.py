@@ -27,7 +27,7 @@ METRICS = {
     "launch__registers_per_thread": "registers_per_thread",
 }
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0,
-         "second": 1e3}
+         "second": 1e3, "ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3}
 
 
 def read(rep, kernel=""):
