@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 import threading
 import weakref
 from dataclasses import dataclass
@@ -193,7 +194,11 @@ def pack_render_args(domain, volume, scene: SceneState, plans: Sequence[SourcePl
         # (exactly reproducible in the reference's float64 order)
         s.iso_exact = 1 if (dim == 1 and all(op in (_abi.OPCODES["add"], _abi.OPCODES["mul"])
                                              for op, _, _ in device_program(plan.chain))) else 0
-        s.range_lo, s.range_hi = (float(v) for v in plan.tf.value_range)
+        prog = device_program(plan.chain)
+        lo, hi = (float(v) for v in plan.tf.value_range)
+        if plan.mode != ISO_MODE:
+            prog, lo, hi = fold_affine_tail(prog, lo, hi)
+        s.range_lo, s.range_hi = lo, hi
         lut = LUTS.get(plan.tf.lut, device)
         keep.append(lut)
         s.lut = ptr(lut)
@@ -207,7 +212,6 @@ def pack_render_args(domain, volume, scene: SceneState, plans: Sequence[SourcePl
             for k, (xk, d) in enumerate(kinks):
                 s.lut_kink_x[k] = xk
                 s.lut_kink_dslope[k][:] = [float(v) for v in d]
-        prog = device_program(plan.chain)
         s.n_steps = len(prog)
         for j, (op, in_dim, arg) in enumerate(prog):
             s.steps[j].op = op
@@ -216,6 +220,38 @@ def pack_render_args(domain, volume, scene: SceneState, plans: Sequence[SourcePl
             s.steps[j].arg_d[:] = [float(v) for v in arg]
             s.step_ops |= (op & 0xF) << (4 * j)
     return a
+
+
+def fold_affine_tail(prog, lo: float, hi: float):
+    """Fold the trailing scalar add / mul steps of a volume source's device
+    program into its classification range.  The chain's last steps map the
+    scalar v to v*M + A (functors.py:212-222); classify_array normalises
+    (v*M + A - lo) / (hi - lo) (scene.py:139-152), which for M > 0 equals
+    (v - lo') / (hi' - lo') with lo' = (lo - A) / M, hi' = lo' + (hi - lo) / M:
+    the same value in real arithmetic (float32 rounding moves the LUT
+    coordinate by a few ulps, far inside the 1e-3 image tolerance), two
+    device steps fewer per sample.  Iso sources keep their chain: their sign
+    tests follow the reference's float64 order exactly (march_multi.cu)."""
+    add_op, mul_op = _abi.OPCODES["add"], _abi.OPCODES["mul"]
+    j = len(prog)
+    while j > 0 and prog[j - 1][0] in (add_op, mul_op) and prog[j - 1][1] == 1:
+        j -= 1
+    if j == len(prog):
+        return prog, lo, hi
+    m, a = 1.0, 0.0
+    for op, _, arg in prog[j:]:
+        c = float(arg[0])
+        if op == mul_op:
+            m, a = m * c, a * c
+        else:
+            a = a + c
+    if not (math.isfinite(m) and math.isfinite(a) and m > 0.0):
+        return prog, lo, hi
+    lo2 = (lo - a) / m
+    hi2 = lo2 + (hi - lo) / m
+    if not (math.isfinite(lo2) and math.isfinite(hi2) and np.float32(lo2) < np.float32(hi2)):
+        return prog, lo, hi
+    return prog[:j], lo2, hi2
 
 
 class _ArgsCache:
@@ -333,6 +369,16 @@ def lut_line(lut: np.ndarray, tol: float = 1e-12):
 _LINE_MAX = {("float", 1, False): 4, ("float", 1, True): 4, ("float", 3, False): 2, ("float", 3, True): 2}
 
 
+def _aos3(arr) -> bool:
+    """float3 field in the interleaved layout the AOS3 gather takes (march.cu aos3_layout)."""
+    try:
+        st = arr.stride()
+        return (len(st) == 4 and st[3] == 1 and st[2] == 3 and st[1] % 2 == 0 and st[0] % 2 == 0
+                and arr.data_ptr() % 8 == 0 and not os.environ.get("ISC_DISABLE_AOS3"))
+    except (AttributeError, TypeError):
+        return False
+
+
 def describe_kernel(plans: Sequence[SourcePlan], settings, analytic_lut: bool = True) -> str:
     """Name of the march kernel ``isc_render_local`` dispatches to for these
     plans (mirrors the library's dispatch; for reports and bench lines)."""
@@ -355,8 +401,9 @@ def describe_kernel(plans: Sequence[SourcePlan], settings, analytic_lut: bool = 
                 line = 1 + len(pw[2])
                 if line > _LINE_MAX.get((elem, dim, bool(et)), 1):
                     line = 0
+            aos3 = ",AOS3=1" if dim == 3 and _aos3(arr) else ""
             return (f"isc::march_fast_kernel<INTERP={int(interp)},GUARDED={int(guarded)},PAIRED=1,"
-                    f"LINE={line},DIM={dim},ET={int(et)},T={elem}>")
+                    f"LINE={line},DIM={dim},ET={int(et)},T={elem}{aos3}>")
     if (len(plans) == 2 and interp and not et and plans[0].mode == ISO_MODE and plans[1].mode != ISO_MODE
             and plans[0].handle.descriptor.feature_dim == 1 and plans[1].handle.descriptor.feature_dim in (1, 3)
             and all(p.handle.descriptor.has_guard for p in plans)
@@ -369,8 +416,10 @@ def describe_kernel(plans: Sequence[SourcePlan], settings, analytic_lut: bool = 
         if line > _LINE_MAX.get(("float", dim, False), 1):
             line = 0
         chain = "1" if plans[0].chain.steps else "0"
+        aos3 = ",AOS3=1" if dim == 3 and _aos3(plans[1].handle.device_view(plans[1].domain)[0]) else ""
         return (f"isc::iso_probe_kernel<CHAIN={chain}> (paired iso probe) + "
-                f"isc::march_fast_kernel<INTERP=1,GUARDED=1,PAIRED=1,LINE={line},DIM={dim},ET=0,T=float> (volume)")
+                f"isc::march_fast_kernel<INTERP=1,GUARDED=1,PAIRED=1,LINE={line},DIM={dim},ET=0,T=float{aos3}> "
+                "(volume)")
     if 1 <= len(plans) <= 4:
         dims = [p.handle.descriptor.feature_dim for p in plans]
         if interp and all(p.handle.descriptor.has_guard for p in plans) and len(plans) <= 2 and \

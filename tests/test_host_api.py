@@ -340,6 +340,10 @@ def test_describe_kernel_mirrors_dispatch():
                        settings=P.RenderSettings(active_set=(0, 1), modes={0: "iso"}))
     assert describe_kernel(build_plans(reg, fr, fr.limits, two), two.settings).startswith(
         "isc::march_multi_fast_kernel<NS=2")
+    split = P.SceneState(camera=one.camera, chain_texts={1: "length"},
+                         settings=P.RenderSettings(active_set=(0, 1), modes={0: "iso"}, early_termination_alpha=1.0))
+    k = describe_kernel(build_plans(reg, fr, fr.limits, split), split.settings)
+    assert k.startswith("isc::iso_probe_kernel<CHAIN=0>") and "DIM=3" in k and "AOS3=1" in k
 
 
 def test_lut_analytic_hinge_form_equals_lut_lerp():
@@ -424,3 +428,34 @@ def test_composite_user_functor_lowers_to_device_steps():
     reg.register_functor(FunctorDescriptor("host_only", False, lambda d: d), {d: (lambda v, c: v) for d in ev})
     with pytest.raises(P.ChainError):
         device_program(P.parse_chain("host_only", reg, None, 2))
+
+
+def test_fold_affine_tail_preserves_normalised_value():
+    """raycast.fold_affine_tail: a volume source's trailing scalar add / mul
+    steps fold into its value range -- (f(v) - lo) / (hi - lo) is unchanged
+    (float64, random chains); mul by a non-positive constant, non-scalar
+    steps and chains without such a tail are left alone."""
+    import math
+    import numpy as np
+    from paper_1611_09048_b200 import _abi
+    from paper_1611_09048_b200.raycast import fold_affine_tail
+    add, mul, length = _abi.OPCODES["add"], _abi.OPCODES["mul"], _abi.OPCODES["length"]
+    rng = np.random.default_rng(5)
+    v = rng.normal(0.0, 3.0, 1000)
+    for _ in range(200):
+        tail = [(int(rng.choice([add, mul])), 1, (float(rng.uniform(0.2, 3.0)), 0.0, 0.0, 0.0))
+                for _ in range(int(rng.integers(1, 4)))]
+        prog = [(length, 3, (0.0,) * 4)] + tail
+        lo, hi = sorted(rng.uniform(-5, 5, 2))
+        out, lo2, hi2 = fold_affine_tail(prog, lo, hi)
+        assert out == prog[:1]
+        f = v.copy()
+        for op, _, arg in tail:
+            f = f * arg[0] if op == mul else f + arg[0]
+        assert np.allclose((f - lo) / (hi - lo), (v - lo2) / (hi2 - lo2), rtol=1e-9, atol=1e-9)
+    neg = [(mul, 1, (-2.0, 0.0, 0.0, 0.0)), (add, 1, (1.0, 0.0, 0.0, 0.0))]
+    assert fold_affine_tail(neg, 0.0, 1.0) == (neg, 0.0, 1.0)
+    vec = [(mul, 3, (2.0, 2.0, 2.0, 0.0)), (length, 3, (0.0,) * 4)]
+    assert fold_affine_tail(vec, 0.0, 1.0) == (vec, 0.0, 1.0)
+    assert fold_affine_tail([], 0.0, 1.0) == ([], 0.0, 1.0)
+    assert math.isclose(fold_affine_tail([(add, 1, (0.5, 0, 0, 0))], 0.0, 1.0)[1], -0.5)
