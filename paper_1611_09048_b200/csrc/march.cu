@@ -101,9 +101,8 @@ __device__ float3 iso_normal(const isc_source& s, const Brick& b, const double p
 // sources, 64-bit element offsets; static 16x16 tiles.
 template <bool INTERP>
 __global__ void __launch_bounds__(kThreads) march_kernel(const __grid_constant__ isc_render_args a) {
-  extern __shared__ float4 lut_s[];
-  for (int i = threadIdx.x; i < a.n_sources * ISC_LUT_ENTRIES; i += blockDim.x)
-    lut_s[i] = reinterpret_cast<const float4*>(a.src[i >> 8].lut)[i & (ISC_LUT_ENTRIES - 1)];
+  extern __shared__ float lut_s[];  // planar tables, kLutWords per source
+  lut_fill_sources(lut_s, a, a.n_sources);
   __syncthreads();
 
   int px, py;
@@ -146,7 +145,7 @@ __global__ void __launch_bounds__(kThreads) march_kernel(const __grid_constant__
         for (int si = 0; si < ns; ++si) {
           const isc_source& s = a.src[si];
           const float cur = scalar_at<false>(s, b, p, INTERP, err);
-          const float4* lut = lut_s + si * ISC_LUT_ENTRIES;
+          const float* lut = lut_s + si * kLutWords;
           const float inv = 1.0f / (s.range_hi - s.range_lo);
           if (s.mode != ISC_ISO) {
             st = over4(st, premultiply(classify(lut, s.range_lo, inv, cur)));
@@ -217,7 +216,7 @@ __global__ void __launch_bounds__(kThreads) march_kernel(const __grid_constant__
       const double d[3] = {r.d[0], r.d[1], r.d[2]};
       const float3 n = iso_normal(s, b, hit_p, d, INTERP, err);
       const float shade = fabsf(n.x * (float)d[0] + n.y * (float)d[1] + n.z * (float)d[2]);
-      const float4 base = classify(lut_s + hit_si * ISC_LUT_ENTRIES, s.range_lo, 1.0f / (s.range_hi - s.range_lo),
+      const float4 base = classify(lut_s + hit_si * kLutWords, s.range_lo, 1.0f / (s.range_hi - s.range_lo),
                                    s.iso_threshold);
       acc = over4(acc, over4(hit_front, make_float4(base.x * shade, base.y * shade, base.z * shade, 1.0f)));
     }
@@ -270,10 +269,9 @@ __global__ void __launch_bounds__(kThreads, ISC_FAST_MINB) march_fast_kernel(con
                                                               const FastField F, int tiles_x, int tiles_y,
                                                               int super_x, int n_codes, int row_order,
                                                               int tw_log2, int tile_x0, int tile_y0) {
-  __shared__ float4 lut_s[ISC_LUT_ENTRIES];
+  __shared__ float lut_s[kLutWords];
   if (LINE == 0 || !PAIRED) {
-    for (int i = threadIdx.x; i < ISC_LUT_ENTRIES; i += blockDim.x)
-      lut_s[i] = reinterpret_cast<const float4*>(a.src[0].lut)[i];
+    lut_fill(lut_s, reinterpret_cast<const float4*>(a.src[0].lut));
     __syncthreads();
   }
 

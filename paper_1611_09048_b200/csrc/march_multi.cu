@@ -300,7 +300,7 @@ __device__ __noinline__ float4 iso_hit_color(const isc_render_args& a, const Mul
   for (int i = 0; i < 3; ++i) hp[i] = dadd(p[i], dmul(tt, d[i]));
   const float3 nrm = multi_normal<INTERP>(M.s[si], M, s, off, isz, hp, d, err);
   const float shade = fabsf(nrm.x * (float)d[0] + nrm.y * (float)d[1] + nrm.z * (float)d[2]);
-  const float4 base = classify(reinterpret_cast<const float4*>(s.lut), s.range_lo, 1.0f / (s.range_hi - s.range_lo),
+  const float4 base = classify_aos(reinterpret_cast<const float4*>(s.lut), s.range_lo, 1.0f / (s.range_hi - s.range_lo),
                                s.iso_threshold);
   return make_float4(base.x * shade, base.y * shade, base.z * shade, 1.0f);
 }
@@ -309,9 +309,8 @@ template <int NS, bool INTERP, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) march_multi_kernel(const __grid_constant__ isc_render_args a,
                                                                const __grid_constant__ MultiField M, int tiles_x,
                                                                int tiles_y, int super_x, int n_codes) {
-  __shared__ float4 lut_s[NS * ISC_LUT_ENTRIES];
-  for (int i = threadIdx.x; i < NS * ISC_LUT_ENTRIES; i += blockDim.x)
-    lut_s[i] = reinterpret_cast<const float4*>(a.src[i >> 8].lut)[i & (ISC_LUT_ENTRIES - 1)];
+  __shared__ float lut_s[NS * kLutWords];
+  lut_fill_sources(lut_s, a, NS);
   __syncthreads();
 
   const int lane = threadIdx.x & 31;
@@ -373,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, MINB) march_multi_kernel(const __gri
           float v[4] = {0.f, 0.f, 0.f, 0.f};
           multi_sample<INTERP>(S, M, ix, iy, iz, fx, fy, fz, v, err);
           const float cur = s.n_steps ? run_chain(s, v, S.dim) : v[0];
-          const float4* lut = lut_s + si * ISC_LUT_ENTRIES;
+          const float* lut = lut_s + si * kLutWords;
           if (s.mode != ISC_ISO) {
             st = over4(st, premultiply(classify(lut, s.range_lo, inv[si], cur)));
             continue;
@@ -553,9 +552,8 @@ __global__ void __launch_bounds__(kMultiFastThreads, ISC_MULTI_FAST_MINB)
     march_multi_fast_kernel(const __grid_constant__ isc_render_args a, const __grid_constant__ MultiField M,
                             int tiles_x, int tiles_y, int super_x, int n_codes, int tile_x0, int tile_y0,
                             int tw_log2) {
-  __shared__ float4 lut_s[NS * ISC_LUT_ENTRIES];
-  for (int i = threadIdx.x; i < NS * ISC_LUT_ENTRIES; i += blockDim.x)
-    lut_s[i] = reinterpret_cast<const float4*>(a.src[i >> 8].lut)[i & (ISC_LUT_ENTRIES - 1)];
+  __shared__ float lut_s[NS * kLutWords];
+  lut_fill_sources(lut_s, a, NS);
   __syncthreads();
 
   const int lane = threadIdx.x & 31;
@@ -680,7 +678,7 @@ __global__ void __launch_bounds__(kMultiFastThreads, ISC_MULTI_FAST_MINB)
           else if (si == 1) cur = run_chain_fast<dim_at<DIMS, 1>()>(s, v[1]);
           else if (si == 2) cur = run_chain_fast<dim_at<DIMS, 2>()>(s, v[2]);
           else cur = run_chain_fast<dim_at<DIMS, 3>()>(s, v[3]);
-          const float4* lut = lut_s + si * ISC_LUT_ENTRIES;
+          const float* lut = lut_s + si * kLutWords;
           const float inv = inv_span[si];
           if (s.mode != ISC_ISO) {
             st = over4(st, classify_src_premul(s, lut, inv, cur));

@@ -67,11 +67,10 @@ __global__ void __launch_bounds__(kStageThreads, 4)
     march_staged_kernel(const __grid_constant__ isc_render_args a, const FastField F, int tiles_x, int tiles_y,
                         int super_x, int n_codes, int tw_log2, int tile_x0, int tile_y0) {
   extern __shared__ float4 smem4[];
-  float4* lut_s = smem4;  // LUT (LINE == 0 only), then the warps' boxes
+  float* lut_s = reinterpret_cast<float*>(smem4);  // planar LUT (LINE == 0 only), then the warps' boxes
   float* boxes = reinterpret_cast<float*>(smem4 + (LINE == 0 ? ISC_LUT_ENTRIES : 0));
   if (LINE == 0) {
-    for (int i = threadIdx.x; i < ISC_LUT_ENTRIES; i += blockDim.x)
-      lut_s[i] = reinterpret_cast<const float4*>(a.src[0].lut)[i];
+    lut_fill(lut_s, reinterpret_cast<const float4*>(a.src[0].lut));
     __syncthreads();
   }
   const int lane = threadIdx.x & 31;

@@ -219,8 +219,8 @@ __device__ __forceinline__ float run_chain_fast(const isc_source& s, float v[4])
   return v[0];
 }
 
-// Straight RGBA from a LUT held in shared memory.
-__device__ __forceinline__ float4 classify(const float4* lut, float lo, float inv_span, float v) {
+// Straight RGBA from a float4 LUT in global memory (iso-hit shading, once per hit).
+__device__ __forceinline__ float4 classify_aos(const float4* lut, float lo, float inv_span, float v) {
   if (!isfinite(v)) return make_float4(0.f, 0.f, 0.f, 0.f);
   float t = (v - lo) * inv_span;
   t = fminf(fmaxf(t, 0.0f), 1.0f);
@@ -231,6 +231,56 @@ __device__ __forceinline__ float4 classify(const float4* lut, float lo, float in
   const float4 a = lut[i0], b = lut[i1];
   return make_float4(fmaf(w, b.x - a.x, a.x), fmaf(w, b.y - a.y, a.y), fmaf(w, b.z - a.z, a.z),
                      fmaf(w, b.w - a.w, a.w));
+}
+
+// Shared-memory LUTs are held planar, one 256-float table per channel
+// (lut_fill): a lookup is eight LDS.32 (both lerp ends of four channels).  A
+// warp's lookups touch a few neighbouring entries, so each LDS.32 is ~1
+// data-pipe wavefront (1.08 measured on C4), while the float4 entry layout's
+// two LDS.128 cost 7.0 each (entries 8 apart share a bank group): C4 LUT path
+// 5.33 -> 4.87 ms, images bit-identical (tools/micro/).
+constexpr int kLutWords = 4 * ISC_LUT_ENTRIES;  // floats per source
+
+// Fill one source's planar table from its float4 LUT (all threads of the CTA;
+// the caller syncs).
+__device__ __forceinline__ void lut_fill(float* dst, const float4* src) {
+  for (int i = threadIdx.x; i < ISC_LUT_ENTRIES; i += blockDim.x) {
+    const float4 c = src[i];
+    dst[0 * ISC_LUT_ENTRIES + i] = c.x;
+    dst[1 * ISC_LUT_ENTRIES + i] = c.y;
+    dst[2 * ISC_LUT_ENTRIES + i] = c.z;
+    dst[3 * ISC_LUT_ENTRIES + i] = c.w;
+  }
+}
+
+// lut_fill for n sources (tables back to back).
+__device__ __forceinline__ void lut_fill_sources(float* dst, const isc_render_args& a, int n) {
+  for (int i = threadIdx.x; i < n * ISC_LUT_ENTRIES; i += blockDim.x) {
+    const float4 c = reinterpret_cast<const float4*>(a.src[i >> 8].lut)[i & (ISC_LUT_ENTRIES - 1)];
+    float* t = dst + (i >> 8) * kLutWords + (i & (ISC_LUT_ENTRIES - 1));
+    t[0 * ISC_LUT_ENTRIES] = c.x;
+    t[1 * ISC_LUT_ENTRIES] = c.y;
+    t[2 * ISC_LUT_ENTRIES] = c.z;
+    t[3 * ISC_LUT_ENTRIES] = c.w;
+  }
+}
+
+// Straight RGBA from a planar LUT in shared memory (scene.py:139-152).
+__device__ __forceinline__ float4 classify(const float* tab, float lo, float inv_span, float v) {
+  if (!isfinite(v)) return make_float4(0.f, 0.f, 0.f, 0.f);
+  float t = (v - lo) * inv_span;
+  t = fminf(fmaxf(t, 0.0f), 1.0f);
+  const float x = t * (float)(ISC_LUT_ENTRIES - 1);
+  const int i0 = min((int)x, ISC_LUT_ENTRIES - 1);
+  const int i1 = min(i0 + 1, ISC_LUT_ENTRIES - 1);
+  const float w = x - (float)i0;
+  float c[4];
+#pragma unroll
+  for (int ch = 0; ch < 4; ++ch) {
+    const float a = tab[ch * ISC_LUT_ENTRIES + i0], b = tab[ch * ISC_LUT_ENTRIES + i1];
+    c[ch] = fmaf(w, b - a, a);
+  }
+  return make_float4(c[0], c[1], c[2], c[3]);
 }
 
 __device__ __forceinline__ float4 premultiply(float4 c) {
@@ -264,7 +314,7 @@ __device__ __forceinline__ float4 classify_line_premul(const isc_source& s, floa
 // piecewise-linear form (isc_source.lut_linear, lut_kinks at run time; see
 // march.cu classify_line_premul for the compile-time variant), else the
 // shared-memory LUT.  Warp-uniform branches.
-__device__ __forceinline__ float4 classify_src_premul(const isc_source& s, const float4* lut, float inv_span,
+__device__ __forceinline__ float4 classify_src_premul(const isc_source& s, const float* lut, float inv_span,
                                                      float v) {
   if (!s.lut_linear) return premultiply(classify(lut, s.range_lo, inv_span, v));
   const float x = fminf(fmaxf((v - s.range_lo) * inv_span, 0.0f), 1.0f) * (float)(ISC_LUT_ENTRIES - 1);

@@ -1,6 +1,8 @@
 """Whole frames at BASELINE sizes against the CPU reference, every pixel.
 
-C2 (512^3 float32, 1920x1080, trilinear + clip plane) and C3 (512^3 scalar
+C2 (512^3 float32, 1920x1080, trilinear + clip plane; linear and 3-point
+transfer functions, each classified analytically and through the
+shared-memory LUT), C4 at N=1 (1024^3) and C3 (512^3 scalar
 iso surface + 512^3 float3 chain length|mul(2)|add(0.1), 1920x1080) are
 rendered on the B200 and by the reference itself (baseline/_ref, else the
 oracle port) on all host cores (tests/fullframe_cpu.py).  Gates: max
@@ -33,24 +35,51 @@ def test_c2_full_frame_vs_reference():
     n = 512
     full = bench.make_field_torch(n, P.GlobalVolume((n, n, n)).local_domain(0, 1), torch.device("cuda"))
     scene = bench.build_scene(P, bench.CONFIGS["c2"])
+    _volume_frame_vs_reference("C2", P, full, n, scene)
+    # 3-point transfer function: hinge-form analytic classification vs LUT
+    _volume_frame_vs_reference("C2 tf_3point", P, full, n, bench.tf3_scene(P, scene))
+
+
+def _volume_frame_vs_reference(name, P, full, n, scene):
+    """One scalar volume frame rendered twice on the GPU -- the analytic
+    transfer function (bench default) and the planar shared-memory LUT
+    (analytic_lut=False) -- both against one CPU render of the reference."""
     vol = P.GlobalVolume((n, n, n))
     dom = vol.local_domain(0, 1)
     reg = P.SourceRegistry(dom)
     reg.register_handle(P.array_backed_handle(P.SourceDescriptor("f", 1, has_guard=True), full, 1))
     P.update_sources(reg, {0}, {})
     fr = P.default_registry()
-    img = P.render_local(P.RankContext(vol, dom, reg, fr, fr.limits), scene, keep_station_counts=True)
-    got = img.pixels.reshape(-1, 4).double().cpu().numpy()
-    counts_gpu = img.station_counts.cpu().numpy().astype(np.int64)
+    ctx = P.RankContext(vol, dom, reg, fr, fr.limits)
+    frames = []
+    for analytic in (True, False):
+        img = P.render_local(ctx, scene, keep_station_counts=True, analytic_lut=analytic)
+        frames.append((analytic, img.pixels.reshape(-1, 4).double().cpu().numpy(),
+                       img.station_counts.cpu().numpy().astype(np.int64), img.stations))
+        del img
     cam = scene.camera
     rgba, counts, kind = render_frame(
-        [dict(array=full.cpu().numpy(), dim=1, tf=scene.tf_points[0], range=(-0.4, 2.4))],
+        [dict(array=full.cpu().numpy(), dim=1, tf=scene.tf_points[0], range=scene.value_ranges[0])],
         dict(position=cam.position, look_at=cam.look_at, size=(W, H)),
         planes=[(p.point, p.normal) for p in scene.clip_planes], n=n)
-    err, flips = _report("C2", kind, got, counts_gpu, rgba, counts)
-    assert err.max() <= 1e-3
-    assert flips == 0
-    assert int(counts.sum()) == img.stations
+    for analytic, got, counts_gpu, stations in frames:
+        err, flips = _report(f"{name} ({'analytic TF' if analytic else 'shared-memory LUT'})", kind, got,
+                             counts_gpu, rgba, counts)
+        assert err.max() <= 1e-3
+        assert flips == 0
+        assert int(counts.sum()) == stations
+
+
+def test_c4_full_frame_vs_reference():
+    """C4 at N=1 (1024^3 float32, 1920x1080; the bench's headline frame):
+    every pixel against the reference, analytic and LUT classification."""
+    import torch
+    import bench
+    import paper_1611_09048_b200 as P
+    n = 1024
+    full = bench.make_field_torch(n, P.GlobalVolume((n, n, n)).local_domain(0, 1), torch.device("cuda"))
+    scene = bench.build_scene(P, bench.CONFIGS["c4"])
+    _volume_frame_vs_reference("C4", P, full, n, scene)
 
 
 def test_c3_full_frame_vs_reference():

@@ -2,6 +2,7 @@
 config: python tools/time_march.py [--config c4] [--reps 20].  With
 ISC_LIB_PATH set it times that library build (A/B experiments)."""
 import argparse
+import hashlib
 import json
 import os
 import sys
@@ -79,6 +80,7 @@ def main():
            "min_ms": round(ms[0], 4), "stations": int(img.stations)}
     chk = out.double().sum().item()
     res["checksum"] = round(chk, 3)
+    res["digest"] = hashlib.sha1(out.cpu().numpy().tobytes()).hexdigest()[:16]  # bit-identity across A/B builds
     print(json.dumps(res))
 
 
