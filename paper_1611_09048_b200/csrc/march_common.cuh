@@ -56,6 +56,18 @@ __device__ __forceinline__ float ldf(const __half* p) { return __half2float(__ld
 __device__ __forceinline__ float ldf(const __nv_bfloat16* p) { return __bfloat162float(__ldg(p)); }
 __device__ __forceinline__ float ldf(const double* p) { return (float)__ldg(p); }
 
+#ifndef ISC_PTR_ADDR
+#define ISC_PTR_ADDR 1
+#endif
+// p + off bytes as one 64-bit add the compiler cannot re-associate into
+// (index + stride) * sizeof(T) address arithmetic.
+template <typename T>
+__device__ __forceinline__ const T* padd(const T* p, long long off) {
+  const T* r;
+  asm("add.s64 %0, %1, %2;" : "=l"(r) : "l"(p), "l"(off));
+  return r;
+}
+
 // CHECK = false: the caller has proven the guard contract for this sample
 // (see march_fast_kernel: endpoint check per ray).
 template <bool INTERP, bool GUARDED, bool CHECK = true, typename T = float>
@@ -100,9 +112,20 @@ __device__ __forceinline__ float fast_sample(const FastField& F, const double p[
       z0 += F.g;
     }
     const T* b = fld + (z0 * F.sz + y0 * F.sy + x0 * F.sx);
+#if ISC_PTR_ADDR
+    // corner addresses as 64-bit pointer adds of byte strides (2 instructions
+    // each) instead of re-forming base + (index + stride) * sizeof(T) per corner
+    const long long bx = (long long)dx * sizeof(T), by = (long long)dy * sizeof(T), bz = (long long)dz * sizeof(T);
+    const T* py = padd(b, by);
+    const T* pz = padd(b, bz);
+    const T* pyz = padd(pz, by);
+    const float v000 = ldf(b), v100 = ldf(padd(b, bx)), v010 = ldf(py), v110 = ldf(padd(py, bx));
+    const float v001 = ldf(pz), v101 = ldf(padd(pz, bx)), v011 = ldf(pyz), v111 = ldf(padd(pyz, bx));
+#else
     const float v000 = ldf(b), v100 = ldf(b + dx), v010 = ldf(b + dy), v110 = ldf(b + dy + dx);
     const T* c = b + dz;
     const float v001 = ldf(c), v101 = ldf(c + dx), v011 = ldf(c + dy), v111 = ldf(c + dy + dx);
+#endif
     const float a0 = fmaf(fx, v100 - v000, v000), a1 = fmaf(fx, v110 - v010, v010);
     const float a2 = fmaf(fx, v101 - v001, v001), a3 = fmaf(fx, v111 - v011, v011);
     const float b0 = fmaf(fy, a1 - a0, a0), b1 = fmaf(fy, a3 - a2, a2);
