@@ -392,21 +392,7 @@ def run_b200(args):
     achieved = float(br.item()) / (kernel_ms_max * 1e-3) / 1e9 / world
     # ncu evidence for this config (profiles/ncu_counters.json, written by
     # tools/ncu_counters.py from one `ncu --set full` capture of the kernel)
-    traffic, l1tex = None, None
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_counters.json")) as fh:
-            rec = json.load(fh).get(f"{args.config}_n{world}")
-        if rec:
-            traffic = rec.get("traffic_bytes")
-            l1tex = {"data_pipe_lsu_frac": round(rec["l1tex_data_pipe_lsu_pct"] / 100.0, 4),
-                     "dram_throughput_frac": round(rec["dram_throughput_pct"] / 100.0, 4),
-                     "issue_active_frac": round(rec["issue_active_pct"] / 100.0, 4),
-                     "l1_hit_rate": round(rec["l1_hit_rate_pct"] / 100.0, 4),
-                     "ncu_kernel_ms": round(rec["duration_ms"], 4), "source": rec["source"],
-                     "note": "the gather's real limiter: L1TEX data-pipe (LSU) wavefronts as a fraction of "
-                             "peak, from the ncu capture named in source (cold, serialised launch)"}
-    except Exception:
-        pass
+    traffic, l1tex = ncu_evidence(f"{args.config}_n{world}")
 
     # e2e through the public API with host buffers: scene bytes in (JSON, as
     # broadcast by the reference runtime) -> LUT + launch block H2D, frame out
@@ -445,7 +431,9 @@ def run_b200(args):
     lut_path = tf_variants = None
     if len(scenes) == 1 and len(active) == 1:
         lut_path = time_tf(scenes[0], False)
-        lut_path["note"] = "same frame, transfer function classified through the 256-entry shared-memory LUT"
+        lut_path["note"] = ("same frame, transfer function classified through the 256-entry shared-memory LUT "
+                            "(planar: one float table per channel)")
+        lut_path["traffic"], lut_path["l1tex"] = ncu_evidence(f"{args.config}_lut_n{world}")
         tf3 = tf3_scene(P, scenes[0])
         tf_variants = {"points": [list(p) for p in TF3_POINTS],
                        "analytic": time_tf(tf3, True), "lut": time_tf(tf3, False),
@@ -567,6 +555,26 @@ def tf3_scene(P, scene):
                         chain_texts=scene.chain_texts, settings=scene.settings, clip_planes=scene.clip_planes)
 
 
+def ncu_evidence(key):
+    """(traffic bytes, l1tex block) for one kernel from profiles/ncu_counters.json
+    (tools/ncu_counters.py: one `ncu --set full` capture of that kernel), or (None, None)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_counters.json")) as fh:
+            rec = json.load(fh).get(key)
+    except (OSError, ValueError):
+        return None, None
+    if not rec:
+        return None, None
+    return rec.get("traffic_bytes"), {
+        "data_pipe_lsu_frac": round(rec["l1tex_data_pipe_lsu_pct"] / 100.0, 4),
+        "dram_throughput_frac": round(rec["dram_throughput_pct"] / 100.0, 4),
+        "issue_active_frac": round(rec["issue_active_pct"] / 100.0, 4),
+        "l1_hit_rate": round(rec["l1_hit_rate_pct"] / 100.0, 4),
+        "ncu_kernel_ms": round(rec["duration_ms"], 4), "source": rec["source"],
+        "note": "the gather's real limiter: L1TEX data-pipe (LSU) wavefronts as a fraction of "
+                "peak, from the ncu capture named in source (cold, serialised launch)"}
+
+
 def time_normalisation(P, torch, reg, domain, peak, reps=10):
     """Per-source normalisation pass (isc_value_range: min/max of the chained
     scalar over the brick interior, warp-shuffle reduction) on source 0."""
@@ -622,7 +630,8 @@ def run_e2e(P, torch, dist, ctx, scene, transport, canvas, order, rank, world, r
     runtime.py:66-67 -- what FrameStreamer ships) and rank 0 copies it into
     pinned host memory on a side stream, overlapped with the next frame
     (double-buffered -- the reference's FrameStreamer overlap,
-    runtime.py:187-249).  The timed region ends after the last D2H landed."""
+    runtime.py:187-249).  Each timed window ends after its last D2H landed;
+    the median of three windows is reported."""
     from paper_1611_09048_b200.device import LUTS
     from paper_1611_09048_b200.runtime import to_rgba8
     w, h = scene.camera.image_size
@@ -657,24 +666,30 @@ def run_e2e(P, torch, dist, ctx, scene, transport, canvas, order, rank, world, r
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    t0.record(stream)
-    for _ in range(steps):
-        one()
-    stream.wait_stream(copy_stream)
-    t1.record(stream)
-    torch.cuda.synchronize()
+    # three back-to-back timed windows of `steps` frames each; the median
+    # window is reported (a host-side stall -- another process, a page-cache
+    # hiccup -- lands in one window and would otherwise set the number)
+    windows = []
+    for _ in range(3):
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(steps):
+            one()
+        stream.wait_stream(copy_stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        tt = torch.tensor([t0.elapsed_time(t1)], dtype=torch.float64, device=red_dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        windows.append(float(tt.item()) / steps)
     gc.enable()
-    ms = t0.elapsed_time(t1)
-    tt = torch.tensor([ms], dtype=torch.float64, device=red_dev)
-    if world > 1:
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    ms_step = float(tt.item()) / steps
+    ms_step = sorted(windows)[1]
     import ctypes
     from paper_1611_09048_b200 import _abi
     h2d = 256 * 4 * 4 + ctypes.sizeof(_abi.RenderArgs)
     return {"value": round(1000.0 / ms_step, 3), "unit": "frames/s", "ms_per_step": round(ms_step, 4),
+            "steps_per_window": steps, "window_ms_per_step": [round(v, 4) for v in windows],
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": (w * h * 4) if rank == 0 else 0,
             "path": "SceneState.from_bytes -> render_local -> binary_swap -> to_rgba8 -> pinned host frame "
                     "(side stream)",

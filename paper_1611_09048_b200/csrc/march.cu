@@ -599,8 +599,10 @@ static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_
   static const bool no_cull = getenv("ISC_DISABLE_CULL") != nullptr;
   const bool culled = !no_cull && brick_screen_rect(a, rx0, ry0, rx1, ry1);
   if (culled) {
-    // pixels outside the rectangle miss the brick: transparent
-    ISC_CUDA_CHECK(cudaMemsetAsync(a->out_rgba, 0, (size_t)a->camera.width * a->camera.height * sizeof(float4), st));
+    // pixels outside the rectangle miss the brick: transparent (nothing to
+    // clear when the rectangle is the whole image)
+    if (!rect_is_whole(a, rx0, ry0, rx1, ry1))
+      ISC_CUDA_CHECK(cudaMemsetAsync(a->out_rgba, 0, (size_t)a->camera.width * a->camera.height * sizeof(float4), st));
     if (rx1 <= rx0 || ry1 <= ry0) return ISC_OK;
   }
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -763,9 +765,16 @@ extern "C" int isc_render_local(const isc_render_args* a, void* stream) {
   int st = validate(a, true);
   if (st != ISC_OK) return st;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (a->error_word) ISC_CUDA_CHECK(cudaMemsetAsync(a->error_word, 0, sizeof(uint32_t), s));
-  if (a->out_station_total) ISC_CUDA_CHECK(cudaMemsetAsync(a->out_station_total, 0, sizeof(unsigned long long), s));
-  if (a->work_counter) ISC_CUDA_CHECK(cudaMemsetAsync(a->work_counter, 0, sizeof(uint32_t), s));
+  // the three per-render accumulators; render_local packs them as one
+  // [stations, error word, tile counter] int64 block: one memset instead of three
+  char* const tot = reinterpret_cast<char*>(a->out_station_total);
+  if (tot && reinterpret_cast<char*>(a->error_word) == tot + 8 && reinterpret_cast<char*>(a->work_counter) == tot + 16) {
+    ISC_CUDA_CHECK(cudaMemsetAsync(tot, 0, 24, s));
+  } else {
+    if (a->error_word) ISC_CUDA_CHECK(cudaMemsetAsync(a->error_word, 0, sizeof(uint32_t), s));
+    if (a->out_station_total) ISC_CUDA_CHECK(cudaMemsetAsync(a->out_station_total, 0, sizeof(unsigned long long), s));
+    if (a->work_counter) ISC_CUDA_CHECK(cudaMemsetAsync(a->work_counter, 0, sizeof(uint32_t), s));
+  }
   FastField F;
   static const bool no_fast = getenv("ISC_DISABLE_FAST") != nullptr;
   if (!no_fast && fast_eligible(a, F)) {

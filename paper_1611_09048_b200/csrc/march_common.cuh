@@ -236,6 +236,12 @@ inline bool brick_screen_rect(const isc_render_args* a, int& x0, int& y0, int& x
   return true;
 }
 
+// The culled rectangle is the whole image: the kernel writes every pixel, so
+// the canvas needs no clearing first.
+inline bool rect_is_whole(const isc_render_args* a, int x0, int y0, int x1, int y1) {
+  return x0 == 0 && y0 == 0 && x1 == a->camera.width && y1 == a->camera.height;
+}
+
 __device__ __forceinline__ int morton3(int w, int shift) {
   return ((w >> shift) & 1) | (((w >> (shift + 2)) & 1) << 1) | (((w >> (shift + 4)) & 1) << 2);
 }

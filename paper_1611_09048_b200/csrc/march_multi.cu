@@ -983,7 +983,9 @@ bool launch_iso_probe(const isc_render_args* a, cudaStream_t st, int* status) {
   static const bool no_cull = getenv("ISC_DISABLE_CULL") != nullptr;
   *status = ISC_OK;
   if (!no_cull && brick_screen_rect(a, rx0, ry0, rx1, ry1, g_split_probe)) {
-    const cudaError_t e = cudaMemsetAsync(a->out_rgba, 0, (size_t)a->camera.width * a->camera.height * sizeof(float4), st);
+    const cudaError_t e = rect_is_whole(a, rx0, ry0, rx1, ry1)
+                              ? cudaSuccess
+                              : cudaMemsetAsync(a->out_rgba, 0, (size_t)a->camera.width * a->camera.height * sizeof(float4), st);
     if (e != cudaSuccess) {
       *status = cuda_fail(e, "cudaMemsetAsync");
       return true;
@@ -1023,7 +1025,8 @@ static int launch_multi_fast(const isc_render_args* a, const MultiField& M, cuda
   int rx0, ry0, rx1, ry1;
   static const bool no_cull = getenv("ISC_DISABLE_CULL") != nullptr;
   if (!no_cull && brick_screen_rect(a, rx0, ry0, rx1, ry1, g_split_probe)) {  // see march.cu launch_fast
-    ISC_CUDA_CHECK(cudaMemsetAsync(a->out_rgba, 0, (size_t)a->camera.width * a->camera.height * sizeof(float4), st));
+    if (!rect_is_whole(a, rx0, ry0, rx1, ry1))
+      ISC_CUDA_CHECK(cudaMemsetAsync(a->out_rgba, 0, (size_t)a->camera.width * a->camera.height * sizeof(float4), st));
     tile_x0 = rx0 / tw;
     tile_y0 = ry0 / th;
     tiles_x = rx1 > rx0 ? (rx1 + tw - 1) / tw - tile_x0 : 0;

@@ -474,7 +474,8 @@ def test_screen_rect_culling_is_exact(multi):
     vec = rng.random((n + 2, n + 2, n + 2, 3)).astype(np.float32)
     vol = P.GlobalVolume((n, n, n), (2, 2, 2))
     cams = [((70.0, 50.0, -40.0), (16.0, 16.0, 16.0)), ((16.0, 90.0, 16.5), (16.0, 16.0, 16.0)),
-            ((-3.0, 5.0, 4.0), (30.0, 20.0, 28.0)), ((15.0, 17.0, 14.0), (0.0, 40.0, 30.0))]
+            ((-3.0, 5.0, 4.0), (30.0, 20.0, 28.0)), ((15.0, 17.0, 14.0), (0.0, 40.0, 30.0)),
+            ((8.0, 8.5, -1.5), (8.0, 8.0, 8.0))]  # brick 0 fills the image: rectangle == whole image
     for r in range(8):
         dom = vol.local_domain(r, 1)
         ox, oy, oz = dom.offset
@@ -496,7 +497,11 @@ def test_screen_rect_culling_is_exact(multi):
                 value_ranges={0: (0.0, 1.0), 1: (0.0, 2.0)}, chain_texts={0: "", 1: "length"},
                 settings=P.RenderSettings(active_set=active, modes={0: "iso"} if multi else {},
                                           iso_thresholds={0: 0.5}, early_termination_alpha=1.0))
-            culled = P.render_local(ctx, scene).pixels.cpu().numpy()
+            # into a NaN-filled canvas: a pixel the culled launch neither
+            # clears nor writes shows up as NaN (the canvas is left uncleared
+            # when the rectangle is the whole image)
+            canvas = torch.full((48, 64, 4), float("nan"), device="cuda")
+            culled = P.render_local(ctx, scene, out=canvas).pixels.cpu().numpy()
             fullraster = P.render_local(ctx, scene, keep_station_counts=True).pixels.cpu().numpy()
             assert np.array_equal(culled, fullraster), (r, pos)
 
