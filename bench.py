@@ -565,14 +565,19 @@ def ncu_evidence(key):
         return None, None
     if not rec:
         return None, None
+    fracs = {"l1tex_data_pipe": rec["l1tex_data_pipe_lsu_pct"] / 100.0, "issue": rec["issue_active_pct"] / 100.0,
+             "dram": rec["dram_throughput_pct"] / 100.0}
     return rec.get("traffic_bytes"), {
-        "data_pipe_lsu_frac": round(rec["l1tex_data_pipe_lsu_pct"] / 100.0, 4),
-        "dram_throughput_frac": round(rec["dram_throughput_pct"] / 100.0, 4),
-        "issue_active_frac": round(rec["issue_active_pct"] / 100.0, 4),
+        "data_pipe_lsu_frac": round(fracs["l1tex_data_pipe"], 4),
+        "dram_throughput_frac": round(fracs["dram"], 4),
+        "issue_active_frac": round(fracs["issue"], 4),
         "l1_hit_rate": round(rec["l1_hit_rate_pct"] / 100.0, 4),
+        "limiter": max(fracs, key=fracs.get),
         "ncu_kernel_ms": round(rec["duration_ms"], 4), "source": rec["source"],
-        "note": "the gather's real limiter: L1TEX data-pipe (LSU) wavefronts as a fraction of "
-                "peak, from the ncu capture named in source (cold, serialised launch)"}
+        "note": "what bounds the kernel (limiter = the busiest of L1TEX data-pipe wavefronts, warp-instruction "
+                "issue and DRAM throughput, each a fraction of its peak) from the ncu capture named in source "
+                "(cold, serialised launch); the gather is served mostly by L1, so the HBM frac above is the "
+                "north star's samples/s figure of merit, not the DRAM load"}
 
 
 def time_normalisation(P, torch, reg, domain, peak, reps=10):

@@ -5,6 +5,8 @@
 # counters file gpurun_out/ncu_counters.json; copy the summaries to
 # profiles/$tag/ and the counters to profiles/ncu_counters.json afterwards
 # (tools/ncu_import.sh).   usage: tools/ncu_all.sh r2 [configs...]
+# A config "cNlut" captures config cN with the shared-memory LUT forced
+# (the bench line's lut_path block reads it as cN_lut_n1).
 set -u
 tag=$1; shift
 cfgs=${*:-c4 c2 c3 c1 c5}
@@ -13,15 +15,17 @@ mkdir -p $out
 for c in $cfgs; do
   # C3 renders in two passes (iso probe + volume march): capture both
   n=1; [ "$c" = c3 ] && n=2
+  base=${c%lut}; extra=""; key=${c}_n1
+  [ "$base" != "$c" ] && { extra="--lut"; key=${base}_lut_n1; }
   ncu --set full --import-source on --clock-control none -k regex:"march|iso_probe" -c $n -f -o $out/$c \
-      python tools/time_march.py --config $c --reps 1 > /dev/null 2>&1
+      python tools/time_march.py --config $base --reps 1 $extra > /dev/null 2>&1
   python tools/ncu_summary.py $out/$c.ncu-rep > $out/march_${c}_ncu.txt
   python tools/ncu_lines.py $out/$c.ncu-rep 30 >> $out/march_${c}_ncu.txt
   if [ "$c" = c3 ]; then
     NCU_COUNTERS=$out/ncu_counters.json python tools/ncu_counters.py c3_n1 $out/$c.ncu-rep profiles/$tag/march_c3_ncu.txt march_fast_kernel
     NCU_COUNTERS=$out/ncu_counters.json python tools/ncu_counters.py c3_probe_n1 $out/$c.ncu-rep profiles/$tag/march_c3_ncu.txt iso_probe
   else
-    NCU_COUNTERS=$out/ncu_counters.json python tools/ncu_counters.py ${c}_n1 $out/$c.ncu-rep profiles/$tag/march_${c}_ncu.txt
+    NCU_COUNTERS=$out/ncu_counters.json python tools/ncu_counters.py $key $out/$c.ncu-rep profiles/$tag/march_${c}_ncu.txt
   fi
   # reports are large; gpurun brings back at most 64 MiB of gpurun_out/
   if [ -z "${NCU_KEEP:-}" ]; then rm -f "gpurun_out/ncu_${tag}/${c}.ncu-rep"; fi
