@@ -428,7 +428,7 @@ def run_b200(args):
                 "roofline_frac": round(float(br.item()) / (float(tl[1]) * 1e-3) / 1e9 / world / peak, 4),
                 "kernel": describe_kernel(plans_v, scene_v.settings, analytic)}
 
-    lut_path = tf_variants = None
+    lut_path = tf_variants = tf4_variants = None
     if len(scenes) == 1 and len(active) == 1:
         lut_path = time_tf(scenes[0], False)
         lut_path["note"] = ("same frame, transfer function classified through the 256-entry shared-memory LUT "
@@ -439,6 +439,11 @@ def run_b200(args):
                        "analytic": time_tf(tf3, True), "lut": time_tf(tf3, False),
                        "note": "same frame with a 3-point transfer function (slope change at t=0.6): analytic "
                                "hinge form (raycast.lut_analytic) vs the shared-memory LUT"}
+        tf4 = tf3_scene(P, scenes[0], TF4_POINTS)
+        tf4_variants = {"points": [list(p) for p in TF4_POINTS],
+                        "analytic": time_tf(tf4, True), "lut": time_tf(tf4, False),
+                        "note": "a 4-point transfer function with both interior points between LUT samples: 4 "
+                                "slope changes, the run-time kink-count variant vs the shared-memory LUT"}
 
     # informational: the same static-view frame replayed as one CUDA graph
     # (FrameGraph: no per-frame host preparation), N=1 only
@@ -491,6 +496,7 @@ def run_b200(args):
                               "per-source analytic form or shared-memory LUT",
             "lut_path": lut_path,
             "tf_3point": tf_variants,
+            "tf_4point": tf4_variants,
             "graph_replay": graph_replay,
             "composite": composite,
             "e2e_host_field": host_field,
@@ -549,9 +555,13 @@ def run_e2e_host_field(P, torch, dist, ctx, scene, transport, canvas, order, ran
 TF3_POINTS = [(0.0, 0.0, 0.0, 0.0, 0.0), (0.6, 0.1, 0.7, 0.4, 0.3), (1.0, 0.7, 1.0, 0.9, 0.8)]
 
 
-def tf3_scene(P, scene):
-    """The scene with C3's 3-point 'cool' transfer function on source 0."""
-    return P.SceneState(camera=scene.camera, tf_points={0: TF3_POINTS}, value_ranges=scene.value_ranges,
+TF4_POINTS = [(0.0, 0.0, 0.0, 0.0, 0.0), (0.21, 0.5, 0.1, 0.1, 0.05), (0.63, 0.1, 0.9, 0.3, 0.4),
+              (1.0, 1.0, 1.0, 1.0, 0.9)]
+
+
+def tf3_scene(P, scene, points=None):
+    """The scene with C3's 3-point 'cool' transfer function (or ``points``) on source 0."""
+    return P.SceneState(camera=scene.camera, tf_points={0: points or TF3_POINTS}, value_ranges=scene.value_ranges,
                         chain_texts=scene.chain_texts, settings=scene.settings, clip_planes=scene.clip_planes)
 
 

@@ -55,15 +55,16 @@
 extern "C" {
 #endif
 
-#define ISC_ABI_VERSION 3  /* 2: isc_render_args.ray_dirs / ray_intervals, isc_gradient_normals;
+#define ISC_ABI_VERSION 4  /* 2: isc_render_args.ray_dirs / ray_intervals, isc_gradient_normals;
                               3: per-slice swap counters, isc_swap_reset, isc_debug_occupy,
                                  isc_render_args.no_layout, piecewise-linear LUTs (lut_kinks),
-                                 float64 iso decisions (iso_exact, iso_threshold_d) */
+                                 float64 iso decisions (iso_exact, iso_threshold_d);
+                              4: ISC_MAX_LUT_KINKS 3 -> 7 (isc_source grows) */
 #define ISC_MAX_SOURCES 8      /* active sources per render                 */
 #define ISC_MAX_CLIP_PLANES 8
 #define ISC_MAX_CHAIN 8        /* ChainLimits.max_length default is 5        */
 #define ISC_LUT_ENTRIES 256    /* scene.py:18                                 */
-#define ISC_MAX_LUT_KINKS 3    /* slope changes of an analytic LUT            */
+#define ISC_MAX_LUT_KINKS 7    /* slope changes of an analytic LUT            */
 #define ISC_MAX_RANKS 64
 #define ISC_MAX_ROUNDS 6       /* log2(ISC_MAX_RANKS)                         */
 #define ISC_IPC_HANDLE_BYTES 64

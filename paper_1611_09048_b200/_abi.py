@@ -16,12 +16,12 @@ from . import errors
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("ISC_LIB_PATH") or os.path.join(_HERE, "lib", "libisaac_b200.so")
 
-ABI_VERSION = 3
+ABI_VERSION = 4
 MAX_SOURCES = 8
 MAX_CLIP_PLANES = 8
 MAX_CHAIN = 8
 LUT_ENTRIES = 256
-MAX_LUT_KINKS = 3
+MAX_LUT_KINKS = 7
 MAX_RANKS = 64
 IPC_HANDLE_BYTES = 64
 MAX_SWAP_CTAS = 1024

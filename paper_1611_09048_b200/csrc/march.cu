@@ -652,6 +652,9 @@ int launch_staged(int lines, const isc_render_args* a, const FastField& F, cudaS
 // shared-memory LUT.  MAXL bounds the template instantiations per variant.
 template <int MAXL, int DIM, bool ET, typename T, bool AOS3 = false>
 static int launch_line(int lines, const isc_render_args* a, const FastField& F, cudaStream_t st) {
+  // 4..ISC_MAX_LUT_KINKS kinks: one variant with the count read at run time
+  if constexpr (MAXL >= 4)
+    if (lines > 4 && lines <= kLineRuntime) return launch_fast<true, true, true, kLineRuntime, DIM, ET, T, AOS3>(a, F, st);
   if (lines > MAXL) lines = 0;
   switch (lines) {
     case 1: return launch_fast<true, true, true, 1, DIM, ET, T, AOS3>(a, F, st);

@@ -294,6 +294,9 @@ __device__ __forceinline__ float4 premultiply(float4 c) {
 // kernel-parameter constants, free FFMA operands).  Returns the
 // PREMULTIPLIED colour; a non-finite value gets alpha 0 (and so rgb 0)
 // through a select instead of a branch.
+// L = kLineRuntime: 4 to ISC_MAX_LUT_KINKS kinks, count read at run time
+// (warp-uniform; one instantiation instead of one per count).
+constexpr int kLineRuntime = ISC_MAX_LUT_KINKS + 1;
 template <int L>
 __device__ __forceinline__ float4 classify_line_premul(const isc_source& s, float lo, float inv_span, float v) {
   const float x = fminf(fmaxf((v - lo) * inv_span, 0.0f), 1.0f) * (float)(ISC_LUT_ENTRIES - 1);
@@ -302,6 +305,7 @@ __device__ __forceinline__ float4 classify_line_premul(const isc_source& s, floa
   for (int ch = 0; ch < 4; ++ch) c[ch] = fmaf(s.lut_slope[ch], x, s.lut_base[ch]);
 #pragma unroll
   for (int k = 0; k < L - 1; ++k) {
+    if (L == kLineRuntime && k >= 3 && k >= s.lut_kinks) break;
     const float h = fmaxf(x - s.lut_kink_x[k], 0.0f);
 #pragma unroll
     for (int ch = 0; ch < 4; ++ch) c[ch] = fmaf(s.lut_kink_dslope[k][ch], h, c[ch]);

@@ -318,7 +318,14 @@ _LINE_CACHE: dict = {}
 _LINE_LOCK = threading.Lock()
 
 
-def lut_analytic(lut: np.ndarray, max_kinks: int = _abi.MAX_LUT_KINKS, tol: float = 1e-12):
+# Most slope changes classified analytically.  The launch block holds up to
+# MAX_LUT_KINKS (7); measured on C4 / C2 (one B200), 4 kinks analytic 4.54 /
+# 0.96 ms vs the shared-memory LUT 4.93 / 1.01, 6 kinks 4.95 / 1.09 -- no
+# better than the LUT from 6 on.
+ANALYTIC_MAX_KINKS = 5
+
+
+def lut_analytic(lut: np.ndarray, max_kinks: int = ANALYTIC_MAX_KINKS, tol: float = 1e-12):
     """(base, slope, kinks) when the LUT lerp -- the piecewise-linear
     interpolant through (i, lut[i]), scene.py:139-152 -- changes slope at no
     more than ``max_kinks`` integer positions: then for x in [0, 255]
@@ -365,8 +372,19 @@ def lut_line(lut: np.ndarray, tol: float = 1e-12):
 
 
 # analytic LUT forms instantiated per (element type, dim, early termination):
-# LINE = 1 + kinks (march.cu dispatch_line)
+# LINE = 1 + kinks (march.cu launch_line); where up to 3 kinks are
+# instantiated, 4..MAX_LUT_KINKS kinks take one variant with the count read
+# at run time (LINE = MAX_LUT_KINKS + 1)
 _LINE_MAX = {("float", 1, False): 4, ("float", 1, True): 4, ("float", 3, False): 2, ("float", 3, True): 2}
+_LINE_RUNTIME = _abi.MAX_LUT_KINKS + 1
+
+
+def _line_variant(kinks: int, elem: str, dim: int, et: bool) -> int:
+    line = 1 + kinks
+    top = _LINE_MAX.get((elem, dim, et), 1)
+    if line <= top:
+        return line
+    return _LINE_RUNTIME if top >= 4 and line <= _LINE_RUNTIME else 0
 
 
 def _aos3(arr) -> bool:
@@ -398,9 +416,7 @@ def describe_kernel(plans: Sequence[SourcePlan], settings, analytic_lut: bool = 
                     _t.bfloat16: "__nv_bfloat16"}.get(dtype, "float")
             line = 0
             if pw is not None and guarded:
-                line = 1 + len(pw[2])
-                if line > _LINE_MAX.get((elem, dim, bool(et)), 1):
-                    line = 0
+                line = _line_variant(len(pw[2]), elem, dim, bool(et))
             aos3 = ",AOS3=1" if dim == 3 and _aos3(arr) else ""
             return (f"isc::march_fast_kernel<INTERP={int(interp)},GUARDED={int(guarded)},PAIRED=1,"
                     f"LINE={line},DIM={dim},ET={int(et)},T={elem}{aos3}>")
@@ -412,9 +428,7 @@ def describe_kernel(plans: Sequence[SourcePlan], settings, analytic_lut: bool = 
         # split render (march.cu launch_split): iso probe, then the volume pass
         pw = lut_analytic(plans[1].tf.lut) if analytic_lut else None
         dim = plans[1].handle.descriptor.feature_dim
-        line = 1 + len(pw[2]) if pw is not None else 0
-        if line > _LINE_MAX.get(("float", dim, False), 1):
-            line = 0
+        line = _line_variant(len(pw[2]), "float", dim, False) if pw is not None else 0
         chain = "1" if plans[0].chain.steps else "0"
         aos3 = ",AOS3=1" if dim == 3 and _aos3(plans[1].handle.device_view(plans[1].domain)[0]) else ""
         return (f"isc::iso_probe_kernel<CHAIN={chain}> (paired iso probe) + "

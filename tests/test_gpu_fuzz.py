@@ -30,9 +30,9 @@ def _random_case(rng):
         u = rng.random()
         if u < 0.3:
             pts = [(0.0, 0.0, 0.0, 0.0, 0.0), (1.0, *rng.random(4))]     # single ramp: analytic path
-        elif u < 0.55:   # 3-4 control points, some on LUT samples: 1-3 kinks (analytic) or more (LUT)
+        elif u < 0.55:   # 3-7 control points, some on LUT samples: 1-7 kinks (analytic) or more (LUT)
             mids = sorted(float(int(rng.integers(20, 236)) / 255.0) if rng.random() < 0.5
-                          else float(rng.uniform(0.08, 0.92)) for _ in range(int(rng.integers(1, 3))))
+                          else float(rng.uniform(0.08, 0.92)) for _ in range(int(rng.integers(1, 6))))
             pts = [(0.0, *rng.random(4)), *[(t, *rng.random(4)) for t in mids], (1.0, *rng.random(4))]
         srcs.append(dict(dim=dim, chain=chain, mode="iso" if iso else "volume", pts=pts,
                          dtype=str(rng.choice(["float32", "float32", "float16", "float64"])) if ns == 1 else "float32"))

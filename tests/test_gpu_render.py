@@ -418,12 +418,17 @@ def test_analytic_single_ramp_classification_equals_lut_path():
     [(0.0, 0.0, 0.1, 0.2, 0.0), (0.6, 0.9, 0.4, 0.1, 0.3), (1.0, 1.0, 1.0, 0.5, 0.8)],       # kink on a sample
     [(0.0, 0.0, 0.1, 0.2, 0.0), (0.37, 0.9, 0.4, 0.1, 0.3), (1.0, 1.0, 1.0, 0.5, 0.8)],      # between samples
     [(0.0, 0.0, 0.0, 0.0, 0.0), (0.2, 0.5, 0.1, 0.1, 0.05), (0.6, 0.1, 0.9, 0.3, 0.4), (1.0, 1.0, 1.0, 1.0, 0.9)],
+    # 4 and 6 slope changes: the run-time kink count variant (LINE = ISC_MAX_LUT_KINKS + 1) and,
+    # beyond ANALYTIC_MAX_KINKS, the shared-memory LUT
+    [(0.0, 0.0, 0.0, 0.0, 0.0), (0.21, 0.5, 0.1, 0.1, 0.05), (0.63, 0.1, 0.9, 0.3, 0.4), (1.0, 1.0, 1.0, 1.0, 0.9)],
+    [(0.0, 0.1, 0.0, 0.2, 0.0), (0.13, 0.6, 0.2, 0.1, 0.2), (0.47, 0.2, 0.8, 0.3, 0.05), (0.81, 0.9, 0.3, 0.7, 0.6),
+     (1.0, 1.0, 1.0, 1.0, 0.9)],
 ])
 @pytest.mark.parametrize("alpha_stop", [1.0, 0.95])
 def test_piecewise_linear_tf_classified_analytically(points, alpha_stop):
-    """tf_from_points LUTs with 1-3 slope changes take the analytic hinge form
-    (base + slope x + sum dslope_k max(x - x_k, 0)); images match the
-    shared-memory LUT path and the CPU oracle."""
+    """tf_from_points LUTs with 1-5 slope changes take the analytic hinge form
+    (base + slope x + sum dslope_k max(x - x_k, 0)), more take the LUT;
+    images match the shared-memory LUT path and the CPU oracle."""
     import paper_1611_09048_b200 as P
     from oracle import isaac_oracle as O
     from paper_1611_09048_b200.raycast import describe_kernel, lut_analytic
@@ -444,9 +449,11 @@ def test_piecewise_linear_tf_classified_analytically(points, alpha_stop):
                          value_ranges={0: (0.1, 0.9)},
                          settings=P.RenderSettings(active_set=(0,), early_termination_alpha=alpha_stop))
     pw = lut_analytic(scene.transfer_function(0).lut)
-    assert pw is not None and 1 <= len(pw[2]) <= 3
+    kinks = lut_analytic(scene.transfer_function(0).lut, max_kinks=7)[2]
+    assert (pw is not None) == (len(kinks) <= 5) and 1 <= len(kinks) <= 7
     plans = P.build_plans(reg, fr, fr.limits, scene)
-    assert f"LINE={1 + len(pw[2])}" in describe_kernel(plans, scene.settings)
+    line = 0 if pw is None else (1 + len(kinks) if len(kinks) <= 3 else 8)
+    assert f"LINE={line}" in describe_kernel(plans, scene.settings)
     fast = P.render_local(ctx, scene).pixels.cpu().numpy()
     lut = P.render_local(ctx, scene, analytic_lut=False).pixels.cpu().numpy()
     # identical up to float32 rounding; with early termination a pixel may

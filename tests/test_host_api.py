@@ -349,20 +349,21 @@ def test_describe_kernel_mirrors_dispatch():
 def test_lut_analytic_hinge_form_equals_lut_lerp():
     """The analytic transfer-function form (raycast.lut_analytic) equals the
     LUT lerp of scene.classify_array (scene.py:139-152) everywhere on
-    [0, 255] for tf_from_points ramps with up to 3 slope changes, and is
+    [0, 255] for tf_from_points ramps with up to ANALYTIC_MAX_KINKS slope changes, and is
     refused (None) beyond that or for non-piecewise LUTs."""
     import numpy as np
     import paper_1611_09048_b200 as P
     from paper_1611_09048_b200.raycast import lut_analytic, lut_line
     rng = np.random.default_rng(3)
-    seen = {0: 0, 1: 0, 2: 0, 3: 0, None: 0}
-    for trial in range(300):
-        k = int(rng.integers(0, 4))
+    seen = {k: 0 for k in range(8)}
+    seen[None] = 0
+    for trial in range(400):
+        k = int(rng.integers(0, 6))
         mids = sorted(float(int(rng.integers(1, 255)) / 255.0) if rng.random() < 0.5 else float(rng.uniform(0.01, 0.99))
                       for _ in range(k))
         pts = [(0.0, *rng.random(4)), *[(t, *rng.random(4)) for t in mids], (1.0, *rng.random(4))]
         lut = P.tf_from_points(pts, (0.0, 1.0)).lut
-        res = lut_analytic(lut)
+        res = lut_analytic(lut, max_kinks=7)
         seen[None if res is None else len(res[2])] += 1
         x = np.concatenate([rng.uniform(0.0, 255.0, 2000), np.arange(256.0)])
         i = np.floor(x).astype(int)
@@ -374,8 +375,10 @@ def test_lut_analytic_hinge_form_equals_lut_lerp():
         got = base[None, :] + slope[None, :] * x[:, None]
         for xk, d in kinks:
             got = got + d[None, :] * np.maximum(x - xk, 0.0)[:, None]
-        assert np.abs(got - want).max() <= 1e-12, (pts, kinks)
-    assert all(seen[c] > 10 for c in (0, 1, 2, 3)) and seen[None] > 10, seen
+        # float64 rounding of the hinge sums (lut_analytic verifies <= 1e-9 at
+        # the samples); far below the float32 the kernels evaluate it in
+        assert np.abs(got - want).max() <= 1e-9, (pts, kinks)
+    assert all(seen[c] > 10 for c in (0, 1, 2, 3, 4)) and seen[None] > 10, seen
     assert lut_line(P.tf_from_points([(0, 0, 0, 0, 0), (1, 1, 1, 1, 1)], (0, 1)).lut) is not None
     noisy = np.sin(np.linspace(0.0, 3.0, 256))[:, None] * np.ones((1, 4))
     assert lut_analytic(noisy) is None

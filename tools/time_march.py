@@ -14,6 +14,7 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 import paper_1611_09048_b200 as P  # noqa: E402
+from paper_1611_09048_b200.raycast import describe_kernel  # noqa: E402
 
 
 def main():
@@ -24,6 +25,8 @@ def main():
     ap.add_argument("--alpha", type=float, default=None, help="early_termination_alpha (default: the config's 1.0)")
     ap.add_argument("--opacity", type=float, default=None, help="scale the transfer function's alpha ramp")
     ap.add_argument("--dtype", default="float32", help="field element type (float32, float16, bfloat16)")
+    ap.add_argument("--points", default=None, help="transfer-function control points of source 0 as JSON, "
+                                                   "e.g. '[[0,0,0,0,0],[0.37,1,0.5,0.2,0.4],[1,1,1,1,1]]'")
     ap.add_argument("--active", default=None, help="comma-separated source ids to render (C3: 0 = iso scalar, "
                                                    "1 = float3 chain)")
     args = ap.parse_args()
@@ -49,6 +52,11 @@ def main():
         pts = {k: [(p[0], p[1], p[2], p[3], p[4] * args.opacity) for p in v] for k, v in scene.tf_points.items()}
         scene = P.SceneState(camera=scene.camera, tf_points=pts, value_ranges=scene.value_ranges,
                              chain_texts=scene.chain_texts, clip_planes=scene.clip_planes, settings=scene.settings)
+    if args.points is not None:
+        pts = [tuple(float(v) for v in p) for p in json.loads(args.points)]
+        scene = P.SceneState(camera=scene.camera, tf_points={**scene.tf_points, 0: pts},
+                             value_ranges=scene.value_ranges, chain_texts=scene.chain_texts,
+                             clip_planes=scene.clip_planes, settings=scene.settings)
     if args.active is not None:
         import dataclasses
         ids = tuple(int(v) for v in args.active.split(","))
@@ -75,6 +83,7 @@ def main():
     torch.cuda.synchronize()
     ms = sorted(a.elapsed_time(b) for a, b in evs)
     res = {"lib": os.environ.get("ISC_LIB_PATH", "default"), "config": args.config, "alpha": args.alpha,
+           "kernel": describe_kernel(plans, scene.settings, analytic_lut=not args.lut),
            "dtype": args.dtype,
            "median_ms": round(ms[len(ms) // 2], 4),
            "min_ms": round(ms[0], 4), "stations": int(img.stations)}
