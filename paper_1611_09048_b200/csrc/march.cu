@@ -119,6 +119,7 @@ __global__ void __launch_bounds__(kThreads) march_kernel(const __grid_constant__
     const Brick b = make_brick(a);
     const double* o = a.camera.origin;
     const bool gate_alpha = a.alpha_stop < 1.0;
+  const float stop_f = __double2float_ru(a.alpha_stop);  // w >= stop_f <=> (double)w >= alpha_stop
     uint32_t* err = a.error_word;
 
     int hit_si = -1;                     // first iso hit, shaded after the loop
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(kThreads) march_kernel(const __grid_constant__
         }
         if (stop) break;
         acc = over4(acc, st);
-        if (gate_alpha && (double)acc.w >= a.alpha_stop) break;
+        if (gate_alpha && acc.w >= stop_f) break;
       }
     }
     if (hit_si >= 0) {  // shaded after the loop: all hitting lanes of the warp together
@@ -279,6 +280,9 @@ __global__ void __launch_bounds__(kThreads, ISC_FAST_MINB) march_fast_kernel(con
   const isc_source& s = a.src[0];
   const float lo = s.range_lo, inv = 1.0f / (s.range_hi - s.range_lo);
   const bool gate_alpha = a.alpha_stop < 1.0;
+  // smallest float f with (double)f >= alpha_stop: for a float w,
+  // w >= stop_f  <=>  (double)w >= alpha_stop (NaN false in both)
+  const float stop_f = __double2float_ru(a.alpha_stop);
   const double* o = a.camera.origin;
   const double step = a.step;
   uint32_t* err = a.error_word;
@@ -404,21 +408,21 @@ __global__ void __launch_bounds__(kThreads, ISC_FAST_MINB) march_fast_kernel(con
           acc = over4(acc, over4(c, odd));
         } else {
           // early termination (raycast.py:377-380): station by station, the
-          // stop test after each one, exactly as the reference's loop
-          if (!parity && !done) {
-            if (left > 0) {
-              acc = over4(acc, c);
-              ++marched;
-              done = (double)acc.w >= a.alpha_stop;
-            }
-            if (!done && left > 1) {
-              acc = over4(acc, odd);
-              ++marched;
-              done = (double)acc.w >= a.alpha_stop;
-            }
-          }
-          done = __shfl_sync(0xffffffffu, done, q) != 0;  // the odd lane follows its pair
-          if (__all_sync(0xffffffffu, done || left <= 2)) break;
+          // stop test after each one, exactly as the reference's loop --
+          // branch-free (every lane evaluates it; only the even lane's
+          // accumulator is used), the float64 test (double)w >= alpha_stop as
+          // the equivalent float32 test w >= stop_f, and the pair's state
+          // passed to the odd lane by ballot (no data-pipe shuffle)
+          const float4 a1 = over4(acc, c), a2 = over4(a1, odd);
+          const bool s1 = left > 0 && !done;
+          const bool d1 = s1 && a1.w >= stop_f;
+          const bool s2 = s1 && !d1 && left > 1;
+          acc = s2 ? a2 : (s1 ? a1 : acc);
+          marched += (uint32_t)s1 + (uint32_t)s2;
+          done = done || d1 || (s2 && a2.w >= stop_f);
+          const unsigned dm = __ballot_sync(0xffffffffu, done);
+          done = (dm >> q) & 1u;  // the odd lane follows its pair
+          if (__ballot_sync(0xffffffffu, !(done || left <= 2)) == 0u) break;
         }
       }
       if constexpr (ET) {
@@ -457,7 +461,7 @@ __global__ void __launch_bounds__(kThreads, ISC_FAST_MINB) march_fast_kernel(con
         acc = over4(acc, premultiply(classify(lut_s, lo, inv, s0)));
         if (gate_alpha) {
           ++stations;
-          if ((double)acc.w >= a.alpha_stop) break;
+          if (acc.w >= stop_f) break;
         }
       }
     }

@@ -315,6 +315,7 @@ __global__ void __launch_bounds__(kThreads, MINB) march_multi_kernel(const __gri
 
   const int lane = threadIdx.x & 31;
   const bool gate_alpha = a.alpha_stop < 1.0;
+  const float stop_f = __double2float_ru(a.alpha_stop);  // w >= stop_f <=> (double)w >= alpha_stop
   const double* o = a.camera.origin;
   const double step = a.step;
   uint32_t* err = a.error_word;
@@ -425,7 +426,7 @@ __global__ void __launch_bounds__(kThreads, MINB) march_multi_kernel(const __gri
         }
         if (stop) break;
         acc = over4(acc, st);
-        if (gate_alpha && (double)acc.w >= a.alpha_stop) break;
+        if (gate_alpha && acc.w >= stop_f) break;
       }
     }
     if (hit_si >= 0) {  // all hitting lanes of the warp shade together
@@ -558,6 +559,7 @@ __global__ void __launch_bounds__(kMultiFastThreads, ISC_MULTI_FAST_MINB)
 
   const int lane = threadIdx.x & 31;
   const bool gate_alpha = a.alpha_stop < 1.0;
+  const float stop_f = __double2float_ru(a.alpha_stop);  // w >= stop_f <=> (double)w >= alpha_stop
   const double* o = a.camera.origin;
   const double step = a.step;
   uint32_t* err = a.error_word;
@@ -738,7 +740,7 @@ __global__ void __launch_bounds__(kMultiFastThreads, ISC_MULTI_FAST_MINB)
           break;
         }
         acc = over4(acc, st);
-        if (gate_alpha && (double)acc.w >= a.alpha_stop) {
+        if (gate_alpha && acc.w >= stop_f) {
           stopped = true;
           break;
         }

@@ -462,3 +462,20 @@ def test_fold_affine_tail_preserves_normalised_value():
     assert fold_affine_tail(vec, 0.0, 1.0) == (vec, 0.0, 1.0)
     assert fold_affine_tail([], 0.0, 1.0) == ([], 0.0, 1.0)
     assert math.isclose(fold_affine_tail([(add, 1, (0.5, 0, 0, 0))], 0.0, 1.0)[1], -0.5)
+
+
+def test_float_stop_threshold_equals_float64_test():
+    """The kernels test early termination as w >= stop_f, stop_f =
+    __double2float_ru(alpha_stop) (the smallest float >= alpha_stop), in
+    place of the reference's float64 (double)w >= alpha_stop
+    (raycast.py:377-380): the two agree for every float w."""
+    import numpy as np
+    rng = np.random.default_rng(5)
+    alphas = np.concatenate([rng.random(2000), [0.99, 0.5, 1.0 - 2.0 ** -30, 2.0 ** -149, 0.1]])
+    for a in alphas:
+        t = np.float32(a)
+        if float(t) < a:
+            t = np.nextafter(t, np.float32(np.inf))
+        w = np.array([np.nextafter(t, np.float32(-np.inf)), t, np.nextafter(t, np.float32(np.inf)), np.float32(a),
+                      np.float32(np.nan)], dtype=np.float32)
+        assert np.array_equal(w >= t, w.astype(np.float64) >= a), a
