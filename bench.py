@@ -403,8 +403,15 @@ def run_b200(args):
     # general shared-memory LUT lookup (no analytic form), and a 3-point
     # transfer function (one slope change: the analytic hinge form, and the
     # same through the LUT) -- what a user steering the TF gets
-    def time_tf(scene_v, analytic):
+    def time_tf(scene_v, analytic, count_stations=False):
         plans_v = P.build_plans(reg, fr, fr.limits, scene_v)
+        bytes_v = br
+        if count_stations:  # the variant marches fewer stations (early termination): its own bytes
+            im = P.render_local(ctx, scene_v, plans=plans_v, out=canvas, analytic_lut=analytic)
+            bytes_v = torch.tensor([float(im.stations * bytes_per_station + w * h * BYTES_PER_PIXEL_OUT)],
+                                   dtype=torch.float64, device=red_dev)
+            if world > 1:
+                dist.all_reduce(bytes_v)
         evs2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
         def frame_v():
             P.render_local(ctx, scene_v, plans=plans_v, out=canvas, check_errors=False, analytic_lut=analytic)
@@ -425,10 +432,10 @@ def run_b200(args):
         if world > 1:
             dist.all_reduce(tl, op=dist.ReduceOp.MAX)
         return {"value": round(1000.0 / float(tl[0]), 3), "unit": "frames/s", "kernel_ms": round(float(tl[1]), 4),
-                "roofline_frac": round(float(br.item()) / (float(tl[1]) * 1e-3) / 1e9 / world / peak, 4),
+                "roofline_frac": round(float(bytes_v.item()) / (float(tl[1]) * 1e-3) / 1e9 / world / peak, 4),
                 "kernel": describe_kernel(plans_v, scene_v.settings, analytic)}
 
-    lut_path = tf_variants = tf4_variants = None
+    lut_path = tf_variants = tf4_variants = et_variant = None
     if len(scenes) == 1 and len(active) == 1:
         lut_path = time_tf(scenes[0], False)
         lut_path["note"] = ("same frame, transfer function classified through the 256-entry shared-memory LUT "
@@ -439,6 +446,19 @@ def run_b200(args):
                        "analytic": time_tf(tf3, True), "lut": time_tf(tf3, False),
                        "note": "same frame with a 3-point transfer function (slope change at t=0.6): analytic "
                                "hinge form (raycast.lut_analytic) vs the shared-memory LUT"}
+        # early termination at the reference's default alpha_stop 0.99
+        # (scene.py:165) with the transfer function's opacity scaled to 0.01
+        # (translucent: rays run deep before they stop)
+        import dataclasses
+        sc0 = scenes[0]
+        et_scene = P.SceneState(camera=sc0.camera, value_ranges=sc0.value_ranges, chain_texts=sc0.chain_texts,
+                                clip_planes=sc0.clip_planes,
+                                tf_points={i: [(p[0], p[1], p[2], p[3], p[4] * 0.01) for p in pts]
+                                           for i, pts in sc0.tf_points.items()},
+                                settings=dataclasses.replace(sc0.settings, early_termination_alpha=0.99))
+        et_variant = time_tf(et_scene, True, count_stations=True)
+        et_variant["note"] = ("same frame, alpha_stop 0.99 (the reference's default) and the transfer function's "
+                              "opacity x0.01; roofline_frac over the stations actually marched")
         tf4 = tf3_scene(P, scenes[0], TF4_POINTS)
         tf4_variants = {"points": [list(p) for p in TF4_POINTS],
                         "analytic": time_tf(tf4, True), "lut": time_tf(tf4, False),
@@ -497,6 +517,7 @@ def run_b200(args):
             "lut_path": lut_path,
             "tf_3point": tf_variants,
             "tf_4point": tf4_variants,
+            "early_termination": et_variant,
             "graph_replay": graph_replay,
             "composite": composite,
             "e2e_host_field": host_field,
