@@ -467,20 +467,27 @@ def run_b200(args):
 
     # informational: the same static-view frame replayed as one CUDA graph
     # (FrameGraph: no per-frame host preparation), N=1 only
+    # (N > 1: every rank replays its captured render + peer-memory swap, the
+    # swap's epoch on the device; max over ranks)
     graph_replay = None
-    if world == 1 and len(scenes) == 1:
+    if len(scenes) == 1 and (world == 1 or isinstance(transport, P.NvlinkTransport)):
         fg = P.FrameGraph(ctx, scenes[0])
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        warm_gpu(fg.replay, seconds=0.05)
-        torch.cuda.synchronize()
+        warm_gpu(fg.replay, dist, world, red_dev, seconds=0.05)
+        barrier()
         g0.record(stream)
         for _ in range(k):
             fg.replay()
         g1.record(stream)
         torch.cuda.synchronize()
-        gms = g0.elapsed_time(g1) / k
+        fg.check()
+        gt = torch.tensor([g0.elapsed_time(g1) / k], dtype=torch.float64, device=red_dev)
+        if world > 1:
+            dist.all_reduce(gt, op=dist.ReduceOp.MAX)
+        gms = float(gt.item())
         graph_replay = {"value": round(1000.0 / gms, 3), "unit": "frames/s", "ms_per_step": round(gms, 4),
-                        "note": "same frame captured once as a CUDA graph (runtime.FrameGraph) and replayed"}
+                        "note": "same frame captured once as a CUDA graph (runtime.FrameGraph: render + "
+                                "binary swap) and replayed"}
 
     norm = time_normalisation(P, torch, reg, domain, peak)
     host_field = None if args.no_host_field_e2e else run_e2e_host_field(

@@ -262,7 +262,9 @@ typedef struct {
   int32_t finish;                /* 1: wait until peers stopped reading  */
   int32_t publish_ready;         /* 1: announce this rank's image ready  */
   int64_t n_pixels;
-  int64_t epoch;                 /* 1, 2, 3, ... identical on all ranks  */
+  int64_t epoch;                 /* 1, 2, 3, ... identical on all ranks;
+                                    0: read it from this rank's flag block
+                                    (isc_swap_epoch_bump; CUDA-graph replayable) */
   int64_t timeout_ns;            /* spin-wait limit -> ISC_E_TRANSPORT   */
   int32_t order[ISC_MAX_RANKS];  /* visibility order (compositing.py:36-63) */
   float* image[ISC_MAX_RANKS];   /* every rank's working image           */
@@ -283,6 +285,12 @@ ISC_API int isc_swap_error_async(unsigned long long* flags, unsigned long long* 
 /* Zero a rank's flag block (stream-ordered).  Collective recovery after a
  * TransportError: every rank resets its own block, then all restart at epoch 1. */
 ISC_API int isc_swap_reset(unsigned long long* flags, void* stream);
+/* Device-resident epoch: add 1 to the epoch word of this rank's flag block
+ * (stream-ordered, one thread).  Called once per logical swap before its
+ * launches with isc_swap_args.epoch = 0, the epoch lives on the device and a
+ * frame's render + swap can be captured as a CUDA graph and replayed (every
+ * rank replaying the same number of times keeps the epochs equal). */
+ISC_API int isc_swap_epoch_bump(unsigned long long* flags, void* stream);
 /* Test aid: occupy the GPU with n_ctas CTAs of `threads` threads that spin
  * for `ns` nanoseconds (a stand-in for the simulation's kernels sharing the
  * GPU with the compositor). */

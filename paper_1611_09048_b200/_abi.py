@@ -167,6 +167,7 @@ _SIGNATURES = {
     "isc_flag_words": (C.c_int, []),
     "isc_swap_status": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int32)]),
     "isc_swap_reset": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "isc_swap_epoch_bump": (C.c_int, [C.c_void_p, C.c_void_p]),
     "isc_swap_error_async": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "isc_debug_occupy": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, C.c_void_p]),
     "isc_arena_alloc": (C.c_int, [C.c_size_t, C.POINTER(C.c_void_p)]),

@@ -238,12 +238,16 @@ def _swap_nvlink(t, pixels, order):
     if pixels.data_ptr() != canvas.data_ptr():
         canvas.copy_(pixels)
     s = stream_handle()
+    # the epoch lives on the device (one bump per swap; the kernel reads it),
+    # so a captured frame replays; the host counter keeps step with it
     t.epoch += 1
-    args = t.swap_args(order)
+    _abi.check(_abi.lib().isc_swap_epoch_bump(C.c_void_p(t.flags[t.rank]), C.c_void_p(s)), "swap epoch")
+    args = t.swap_args(order, epoch=0)
     fn = _abi.lib().isc_binary_swap if (t.size & (t.size - 1)) == 0 else _abi.lib().isc_direct_send
     _abi.check(fn(C.byref(args), C.c_void_p(s)), "binary_swap")
     _account(t, order)
-    t.check_errors(s)
+    if not t.capturing:     # inside a CUDA-graph capture: FrameGraph.check() reads the error word
+        t.check_errors(s)
     if t.rank == 0:
         return t.root_output(h, w).clone()
     return None
@@ -263,12 +267,13 @@ def binary_swap_local(group, images, order):
         raise CompositeError("every rank must cut the image into the same number of slices (n_ctas)")
     shape = tuple(images[0].shape)
     h, w = shape[0], shape[1]
+    s = stream_handle()
+    lib = _abi.lib()
     for r, ep in enumerate(eps):
         canvas = ep.canvas(h, w)
         canvas.copy_(images[r])
-        ep.epoch += 1
-    s = stream_handle()
-    lib = _abi.lib()
+        ep.epoch += 1       # host and device epochs in step (launches below pass the host value)
+        _abi.check(lib.isc_swap_epoch_bump(C.c_void_p(ep.flags[ep.rank]), C.c_void_p(s)), "swap epoch")
     if size == 1:
         return images[0].clone()
     if size & (size - 1):

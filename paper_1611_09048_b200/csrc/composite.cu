@@ -43,6 +43,7 @@ namespace isc {
 // epoch, so "stage reached in epoch e" is "counter >= e".
 constexpr int kCtrlWords = 16;
 constexpr int kErrWord = 9;
+constexpr int kEpochWord = 10;  // device-resident epoch (isc_swap_epoch_bump)
 constexpr int kStages = ISC_SWAP_STAGES;
 constexpr int kRootReadStage = kStages - 1;
 constexpr int kFlagWords = kCtrlWords + kStages * ISC_MAX_SWAP_CTAS;
@@ -172,7 +173,7 @@ __global__ void __launch_bounds__(512) swap_kernel(const __grid_constant__ isc_s
   int rounds = 0;
   while ((1 << rounds) < R) ++rounds;
   unsigned long long* me = a.flags[a.rank];
-  const unsigned long long target = (unsigned long long)a.epoch;
+  const unsigned long long target = a.epoch ? (unsigned long long)a.epoch : __ldcg(me + kEpochWord);
   float4* mine = reinterpret_cast<float4*>(a.image[a.rank]);
 
   // slice b of the image is ready (stream-ordered after the render)
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(512) swap_kernel(const __grid_constant__ isc_s
 __global__ void __launch_bounds__(512) direct_send_kernel(const __grid_constant__ isc_swap_args a) {
   const int b = blockIdx.x;
   unsigned long long* me = a.flags[a.rank];
-  const unsigned long long target = (unsigned long long)a.epoch;
+  const unsigned long long target = a.epoch ? (unsigned long long)a.epoch : __ldcg(me + kEpochWord);
   if (a.publish_ready) publish(stage_word(me, 0, b));
   long long c0, c1;
   slice_of(a.n_pixels, a.n_ctas, b, c0, c1);
@@ -255,7 +256,7 @@ static int check_swap(const isc_swap_args* a, bool pow2) {
   if (a->rank < 0 || a->rank >= a->size) return fail(ISC_E_COMPOSITE, "rank out of range");
   if (pow2 && (a->size & (a->size - 1))) return fail(ISC_E_COMPOSITE, "binary swap needs a power-of-two size");
   if (a->n_ctas < 1 || a->n_ctas > ISC_MAX_SWAP_CTAS) return fail(ISC_E_COMPOSITE, "n_ctas out of range");
-  if (a->epoch < 1) return fail(ISC_E_COMPOSITE, "epoch must start at 1");
+  if (a->epoch < 0) return fail(ISC_E_COMPOSITE, "epoch must be >= 1 (or 0: device-resident)");
   unsigned seen = 0;
   unsigned long long seen_hi = 0;
   for (int i = 0; i < a->size; ++i) {
@@ -343,6 +344,15 @@ extern "C" int isc_swap_reset(unsigned long long* flags, void* stream) {
   if (!flags) return fail(ISC_E_VALUE, "null flag block");
   ISC_CUDA_CHECK(cudaMemsetAsync(flags, 0, sizeof(unsigned long long) * kFlagWords,
                                  reinterpret_cast<cudaStream_t>(stream)));
+  return ISC_OK;
+}
+
+__global__ void epoch_bump_kernel(unsigned long long* flags) { flags[kEpochWord] += 1ull; }
+
+extern "C" int isc_swap_epoch_bump(unsigned long long* flags, void* stream) {
+  if (!flags) return fail(ISC_E_VALUE, "null flag block");
+  epoch_bump_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(flags);
+  ISC_CUDA_CHECK(cudaGetLastError());
   return ISC_OK;
 }
 

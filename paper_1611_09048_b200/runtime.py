@@ -397,25 +397,35 @@ def frame_pipeline(ctx: PipelineContext, frame_payload: dict) -> Optional[FrameR
 class FrameGraph:
     """A static view's frame (``render_local`` + ``binary_swap``) captured once
     as a CUDA graph and replayed per frame -- no host preparation, one graph
-    launch.  For one rank (``LocalFabric`` of size 1 / no transport): the
-    peer-memory swap's epoch handshake is host state and cannot be replayed.
+    launch per rank.  One rank (``LocalFabric`` of size 1 / no transport), or
+    every rank of an ``NvlinkTransport``: the peer-memory swap keeps its
+    epoch on the device (``isc_swap_epoch_bump``), so the captured swap
+    replays; construction and every ``replay()`` are then collective (all
+    ranks, same count, as ``binary_swap``).  Byte transports are not
+    replayable.
 
     The fields are read in place at replay time (zero-copy, as every render);
     the scene, plans, transfer functions and the brick's device arrays must
-    stay the ones captured.  ``replay()`` returns the frame tensor, which the
-    next replay overwrites (``frame`` is that same tensor).
+    stay the ones captured.  ``replay()`` returns the frame tensor (rank 0;
+    ``None`` on other ranks of a swap), which the next replay overwrites.
+    ``check()`` raises the last replay's guard-contract error and any swap
+    spin-wait timeout since the previous check.
     """
 
     def __init__(self, rank_ctx, scene: SceneState, warmup: int = 4):
         import torch
         from .raycast import build_plans, render_local
+        from .transport import NvlinkTransport
         tr = rank_ctx.transport
-        if tr is not None and getattr(tr, "size", 1) != 1:
-            raise ValueError("FrameGraph replays one rank's frame; multi-rank swaps are not replayable")
+        multi = tr is not None and getattr(tr, "size", 1) != 1
+        if multi and not isinstance(tr, NvlinkTransport):
+            raise ValueError("FrameGraph replays a multi-rank frame only over an NvlinkTransport "
+                             "(byte transports run on the host)")
+        self._tr = tr if multi else None
         self.plans = build_plans(rank_ctx.registry, rank_ctx.functor_registry, rank_ctx.limits, scene)
         w, h = scene.camera.image_size
         dev = torch.device("cuda", torch.cuda.current_device())
-        self.canvas = torch.empty((h, w, 4), dtype=torch.float32, device=dev)
+        self.canvas = tr.canvas(h, w) if multi else torch.empty((h, w, 4), dtype=torch.float32, device=dev)
         order = visibility_order(rank_ctx.global_volume, scene.camera)
         self._stream = torch.cuda.Stream()
 
@@ -430,10 +440,30 @@ class FrameGraph:
                 frame()
                 self._stream.synchronize()
         self._last.check()
-        self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph, stream=self._stream):
-            self.frame = frame()
+        if multi:
+            tr.flush()
+            tr.capturing = True
+        try:
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph, stream=self._stream):
+                self.frame = frame()
+        finally:
+            if multi:
+                tr.capturing = False
 
     def replay(self):
         self.graph.replay()
+        if self._tr is not None:
+            self._tr.epoch += 1     # the replayed swap bumped the device epoch
         return self.frame
+
+    def check(self) -> None:
+        """Synchronise and raise GuardContractError / TransportError if a
+        replay hit one (the errors of all replays since the last check)."""
+        import torch
+        from .device import stream_handle
+        self._stream.wait_stream(torch.cuda.current_stream())
+        torch.cuda.current_stream().wait_stream(self._stream)
+        self._last.check()
+        if self._tr is not None:
+            self._tr.status(stream_handle())

@@ -342,6 +342,7 @@ class NvlinkTransport(_HostCollectives):
             self.root_out = root_base + self.arena.image_bytes
         self.n_pixels = self.arena.n_pixels
         self.epoch = 0
+        self.capturing = False        # set by FrameGraph while a frame is captured
         self._status_host = torch.zeros(1, dtype=torch.int64).pin_memory()   # allocated up front
         self._err_slots = [torch.zeros(1, dtype=torch.int64).pin_memory() for _ in range(4)]
         self._pending: list = []      # (event, slot) of deferred error checks
@@ -381,7 +382,7 @@ class NvlinkTransport(_HostCollectives):
         a.finish = kw.get("finish", 1)
         a.publish_ready = kw.get("publish_ready", 1)
         a.n_pixels = self.n_pixels
-        a.epoch = self.epoch
+        a.epoch = kw.get("epoch", self.epoch)     # 0: the device-resident epoch (isc_swap_epoch_bump)
         a.timeout_ns = int(kw.get("timeout_s", self.timeout_s) * 1e9)
         for i in range(self.size):
             a.order[i] = int(order[i])

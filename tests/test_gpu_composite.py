@@ -291,3 +291,26 @@ def test_swap_timeout_deferred_check():
         ep.flush()   # the error word was cleared: nothing pending
     finally:
         grp.close()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_multi_rank_frame_graph_replays(world):
+    """A static view captured as a multi-rank FrameGraph (render + fused
+    peer-memory swap; the swap reads its epoch from the device) replays
+    bit-identically to render_local + binary_swap, with plain swaps
+    interleaved (torchrun, process per rank, all on one GPU)."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    helper = os.path.join(os.path.dirname(os.path.abspath(__file__)), "helpers", "mp_framegraph.py")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", helper, "5"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=400)
+    assert out.returncode == 0, out.stderr[-3000:]
+    res = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert res["all_identical"] and res["checks"] == 7 and res["nonzero"] > 0, res

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--dtype", default="float32", help="field element type (float32, float16, bfloat16)")
     ap.add_argument("--points", default=None, help="transfer-function control points of source 0 as JSON, "
                                                    "e.g. '[[0,0,0,0,0],[0.37,1,0.5,0.2,0.4],[1,1,1,1,1]]'")
+    ap.add_argument("--volume-only", action="store_true", help="every source in volume mode (no iso)")
     ap.add_argument("--active", default=None, help="comma-separated source ids to render (C3: 0 = iso scalar, "
                                                    "1 = float3 chain)")
     args = ap.parse_args()
@@ -52,6 +53,11 @@ def main():
         pts = {k: [(p[0], p[1], p[2], p[3], p[4] * args.opacity) for p in v] for k, v in scene.tf_points.items()}
         scene = P.SceneState(camera=scene.camera, tf_points=pts, value_ranges=scene.value_ranges,
                              chain_texts=scene.chain_texts, clip_planes=scene.clip_planes, settings=scene.settings)
+    if args.volume_only:
+        import dataclasses
+        scene = P.SceneState(camera=scene.camera, tf_points=scene.tf_points, value_ranges=scene.value_ranges,
+                             chain_texts=scene.chain_texts, clip_planes=scene.clip_planes,
+                             settings=dataclasses.replace(scene.settings, modes={}))
     if args.points is not None:
         pts = [tuple(float(v) for v in p) for p in json.loads(args.points)]
         scene = P.SceneState(camera=scene.camera, tf_points={**scene.tf_points, 0: pts},
