@@ -479,3 +479,19 @@ def test_float_stop_threshold_equals_float64_test():
         w = np.array([np.nextafter(t, np.float32(-np.inf)), t, np.nextafter(t, np.float32(np.inf)), np.float32(a),
                       np.float32(np.nan)], dtype=np.float32)
         assert np.array_equal(w >= t, w.astype(np.float64) >= a), a
+
+
+def test_frame_graph_refuses_byte_transports():
+    """runtime.FrameGraph replays a multi-rank frame only over an
+    NvlinkTransport (device-resident swap epoch); a byte transport with more
+    than one rank is refused before any device work."""
+    import pytest
+    import paper_1611_09048_b200 as P
+    vol = P.GlobalVolume((8, 8, 8), (2, 1, 1))
+    dom = vol.local_domain(0, 1)
+    reg = P.SourceRegistry(dom)
+    fr = P.default_registry()
+    ctx = P.RankContext(vol, dom, reg, fr, fr.limits, P.LocalFabric(2).endpoint(0))
+    scene = P.SceneState(camera=P.Camera((30.0, 4.0, 4.0), (4.0, 4.0, 4.0), image_size=(8, 8)))
+    with pytest.raises(ValueError, match="NvlinkTransport"):
+        P.FrameGraph(ctx, scene)
