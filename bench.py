@@ -459,9 +459,12 @@ def run_b200(args):
         et_variant = time_tf(et_scene, True, count_stations=True)
         et_variant["note"] = ("same frame, alpha_stop 0.99 (the reference's default) and the transfer function's "
                               "opacity x0.01; roofline_frac over the stations actually marched")
+        et_variant["traffic"], et_variant["l1tex"] = ncu_evidence(f"{args.config}_et_n{world}")
         tf4 = tf3_scene(P, scenes[0], TF4_POINTS)
         tf4_variants = {"points": [list(p) for p in TF4_POINTS],
-                        "analytic": time_tf(tf4, True), "lut": time_tf(tf4, False),
+                        "analytic": dict(time_tf(tf4, True),
+                                         l1tex=ncu_evidence(f"{args.config}_tf4_n{world}")[1]),
+                        "lut": time_tf(tf4, False),
                         "note": "a 4-point transfer function with both interior points between LUT samples: 4 "
                                 "slope changes, the run-time kink-count variant vs the shared-memory LUT"}
 
