@@ -127,6 +127,24 @@ def test_inactive_sources_never_touched():
         assert ctx.registry.handle(2).sample_count == 0
 
 
+def test_sample_count_over_many_renders():
+    """sample_count over a long render loop (device counters folded on the
+    device every 64 renders, no host sync) = renders x stations x 8 taps."""
+    import paper_1611_09048_b200 as P
+    from product_build import product_ctx, product_scene
+    c = cases.case("c1")
+    scene = product_scene(c)
+    ctx = product_ctx(c, (1, 1, 1), 0)
+    h = ctx.registry.handle(0)
+    h.sample_count = 0
+    first = P.render_local(ctx, scene, check_errors=False)
+    for _ in range(149):
+        P.render_local(ctx, scene, check_errors=False)
+    assert h.sample_count == 150 * first.stations * 8
+    P.render_local(ctx, scene, check_errors=False)
+    assert h.sample_count == 151 * first.stations * 8
+
+
 def test_offscreen_is_transparent_and_energy_bound():
     import paper_1611_09048_b200 as P
     from product_build import product_ctx, product_scene
