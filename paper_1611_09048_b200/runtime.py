@@ -460,10 +460,7 @@ class FrameGraph:
     def check(self) -> None:
         """Synchronise and raise GuardContractError / TransportError if a
         replay hit one (the errors of all replays since the last check)."""
-        import torch
         from .device import stream_handle
-        self._stream.wait_stream(torch.cuda.current_stream())
-        torch.cuda.current_stream().wait_stream(self._stream)
-        self._last.check()
+        self._last.check()          # replays run on the current stream; this reads after them
         if self._tr is not None:
             self._tr.status(stream_handle())
