@@ -14,13 +14,13 @@ next frame renders (FrameStreamer overlap, runtime.py:187-249).
 from __future__ import annotations
 
 import base64
+import concurrent.futures
 import ctypes as C
 import dataclasses
 import io
 import json
 import logging
 import queue
-import threading
 import time
 from dataclasses import dataclass, field
 from typing import Callable, Optional, Sequence
@@ -66,17 +66,36 @@ def to_rgba8(image, stream=None):
     return out
 
 
+def _png_bytes(rgba8: np.ndarray) -> bytes:
+    from PIL import Image
+    out = io.BytesIO()
+    Image.fromarray(rgba8, mode="RGBA").save(out, format="PNG")
+    return out.getvalue()
+
+
+def _png_array(blob: bytes, width: int, height: int) -> np.ndarray:
+    from PIL import Image
+    return np.asarray(Image.open(io.BytesIO(blob)).convert("RGBA"))
+
+
+# frame codecs of the reference's wire format (runtime.py:45-81): uint8
+# (H, W, 4) frame <-> payload bytes; base64 on top for the message
+_CODECS = {
+    RAW_RGBA8: (lambda a: a.tobytes(),
+                lambda blob, w, h: np.frombuffer(blob, dtype=np.uint8).reshape(h, w, 4)),
+    PNG: (_png_bytes, _png_array),
+}
+
+
+def _codec(encoding: str):
+    try:
+        return _CODECS[encoding]
+    except KeyError:
+        raise ValueError(f"unknown frame encoding {encoding!r}") from None
+
+
 def _encode_bytes(data: np.ndarray, encoding: str) -> str:
-    if encoding == RAW_RGBA8:
-        raw = data.tobytes()
-    elif encoding == PNG:
-        from PIL import Image
-        buf = io.BytesIO()
-        Image.fromarray(data, mode="RGBA").save(buf, format="PNG")
-        raw = buf.getvalue()
-    else:
-        raise ValueError(f"unknown frame encoding {encoding!r}")
-    return base64.b64encode(raw).decode("ascii")
+    return base64.b64encode(_codec(encoding)[0](data)).decode("ascii")
 
 
 def encode_frame(image, encoding: str = RAW_RGBA8, quality: Optional[int] = None) -> str:
@@ -85,13 +104,9 @@ def encode_frame(image, encoding: str = RAW_RGBA8, quality: Optional[int] = None
 
 
 def decode_frame(data: str, width: int, height: int, encoding: str = RAW_RGBA8) -> np.ndarray:
-    raw = base64.b64decode(data)
-    if encoding == RAW_RGBA8:
-        return np.frombuffer(raw, dtype=np.uint8).reshape(height, width, 4)
-    if encoding == PNG:
-        from PIL import Image
-        return np.asarray(Image.open(io.BytesIO(raw)).convert("RGBA"))
-    raise ValueError(f"unknown frame encoding {encoding!r}")
+    """Inverse of encode_frame (runtime.py:70-78)."""
+    unpack = _codec(encoding)[1]
+    return unpack(base64.b64decode(data), width, height)
 
 
 def merge_metadata(per_rank_docs: Sequence[dict]) -> dict:
@@ -127,8 +142,10 @@ class FrameStreamer:
         self.encoding = encoding
         self.quality = quality
         self.timeline: list = []
-        self._pending: Optional[threading.Thread] = None
-        self._failure: Optional[BaseException] = None
+        # one background worker, at most one frame in flight: the future of
+        # the frame being sent (its exception re-raised at the rendezvous)
+        self._worker = concurrent.futures.ThreadPoolExecutor(max_workers=1, thread_name_prefix="frame-send")
+        self._inflight: Optional[concurrent.futures.Future] = None
         self._stream = torch.cuda.Stream()
         self._host = None
 
@@ -136,16 +153,13 @@ class FrameStreamer:
         self.timeline.append((event, step, time.monotonic()))
 
     def wait_previous(self) -> None:
-        if self._pending is not None:
-            self._pending.join()
-            self._pending = None
-        if self._failure is not None:
-            failure, self._failure = self._failure, None
-            raise failure
+        job, self._inflight = self._inflight, None
+        if job is not None:
+            job.result()
 
     def submit(self, frame, step: int, metadata: dict, scene: SceneState) -> None:
         import torch
-        if self._pending is not None:
+        if self._inflight is not None:
             raise RuntimeError("previous frame still in flight; wait_previous() first")
         q = to_rgba8(frame)
         ready = torch.cuda.Event()
@@ -159,29 +173,25 @@ class FrameStreamer:
             q.record_stream(self._stream)
         copied = torch.cuda.Event()
         copied.record(self._stream)
-        h, w = int(q.shape[0]), int(q.shape[1])
-        scene_doc = scene.to_json()
+        message = {"type": "frame", "step": step,
+                   "image": {"width": int(q.shape[1]), "height": int(q.shape[0]), "encoding": self.encoding},
+                   "metadata": metadata, "scene": scene.to_json()}
+        self._inflight = self._worker.submit(self._send, message, host, copied, step)
 
-        def job():
-            try:
-                self.mark("send_begin", step)
-                copied.synchronize()
-                self.sink({"type": "frame", "step": step,
-                           "image": {"width": w, "height": h, "encoding": self.encoding,
-                                     "data": self.encoder(host.numpy(), self.encoding, self.quality)},
-                           "metadata": metadata, "scene": scene_doc})
-            except BaseException as exc:  # noqa: BLE001 -- surfaced at the rendezvous
-                self._failure = exc
-            finally:
-                self.mark("send_end", step)
-
-        self._pending = threading.Thread(target=job, daemon=True)
-        self._pending.start()
+    def _send(self, message: dict, host, copied, step: int) -> None:
+        self.mark("send_begin", step)
+        try:
+            copied.synchronize()            # the frame's D2H landed in pinned memory
+            message["image"]["data"] = self.encoder(host.numpy(), self.encoding, self.quality)
+            self.sink(message)
+        finally:
+            self.mark("send_end", step)
 
     def close(self) -> None:
-        if self._pending is not None:
-            self._pending.join()
-            self._pending = None
+        job, self._inflight = self._inflight, None
+        if job is not None:
+            concurrent.futures.wait([job])
+        self._worker.shutdown(wait=True)
 
 
 CONTROL_ACTIONS = ("pause", "resume", "step", "exit")
@@ -305,12 +315,15 @@ class PipelineContext:
     steering_unknown: int = 0
 
     def drain_inbox(self) -> list:
-        out = []
-        while True:
+        """Every steering message queued so far (non-blocking; later arrivals
+        wait for the next frame)."""
+        got = []
+        for _ in range(self.inbox.qsize()):
             try:
-                out.append(self.inbox.get_nowait())
+                got.append(self.inbox.get_nowait())
             except queue.Empty:
-                return out
+                break
+        return got
 
     @property
     def rank(self) -> int:
