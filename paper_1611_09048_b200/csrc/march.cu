@@ -22,6 +22,7 @@
 #include "common.cuh"
 #include "launch_tuner.cuh"
 #include <mutex>
+#include <type_traits>
 
 #include "march_common.cuh"
 #include "raysetup.cuh"
@@ -264,8 +265,12 @@ __global__ void __launch_bounds__(kThreads) march_kernel(const __grid_constant__
 // LINE: 0 = transfer function read from the shared-memory LUT, L >= 1 =
 // analytic piecewise-linear form with L-1 kinks (classify_line_premul<L>).
 // AOS3: float3 source in the standard interleaved layout (fast_gather_aos3).
+// LANES (paired only): lanes per ray -- 2 (the paired march: 16 rays x 2
+// station parities) or 4 for small frames (8 rays x 4 parities, merged by a
+// two-level shuffle tree): with fewer tiles than resident warps the launch
+// lasts as long as its longest ray, and 4 lanes halve that serial path.
 template <bool INTERP, bool GUARDED, bool PAIRED, int LINE = 0, int DIM = 1, bool ET = false,
-          typename T = float, bool AOS3 = false>
+          typename T = float, bool AOS3 = false, int LANES = 2>
 __global__ void __launch_bounds__(kThreads, ISC_FAST_MINB) march_fast_kernel(const __grid_constant__ isc_render_args a,
                                                               const FastField F, int tiles_x, int tiles_y,
                                                               int super_x, int n_codes, int row_order,
@@ -288,9 +293,11 @@ __global__ void __launch_bounds__(kThreads, ISC_FAST_MINB) march_fast_kernel(con
   uint32_t* err = a.error_word;
   unsigned long long warp_stations = 0;
   const int tw = 1 << tw_log2;
-  const int th = (PAIRED ? 16 : 32) >> tw_log2;
-  const int q = PAIRED ? (lane & 15) : lane;
-  const int parity = PAIRED ? (lane >> 4) : 0;
+  static_assert(LANES == 2 || (LANES == 4 && PAIRED && !ET), "4 lanes per ray: paired, no early termination");
+  constexpr int kRays = PAIRED ? 32 / LANES : 32;  // rays per warp
+  const int th = kRays >> tw_log2;
+  const int q = lane & (kRays - 1);
+  const int parity = PAIRED ? lane / kRays : 0;
 
   for (;;) {
     int t = 0;
@@ -371,16 +378,16 @@ __global__ void __launch_bounds__(kThreads, ISC_FAST_MINB) march_fast_kernel(con
         }
       }
       constexpr bool kCheck = false;
-      const unsigned pairs = (unsigned)((nm + 1) >> 1);
+      const unsigned pairs = (unsigned)((nm + LANES - 1) / LANES);
       const unsigned trips = __reduce_max_sync(0xffffffffu, pairs);
-      // station index as an exact float64 integer (k < 2^53) stepped by 2.0:
-      // no int64 -> float64 conversion per sample; `left` counts this lane's
-      // remaining stations.
+      // station index as an exact float64 integer (k < 2^53) stepped by
+      // LANES: no int64 -> float64 conversion per sample; `left` counts this
+      // lane's remaining stations.
       double kd = (double)(r.k_lo + parity);
       int left = (int)nm - parity;
       bool done = false;        // ET: the pair's ray reached alpha_stop
       uint32_t marched = 0;     // ET: stations composited (even lane)
-      for (unsigned j = 0; j < trips; ++j, left -= 2, kd = dadd(kd, 2.0)) {
+      for (unsigned j = 0; j < trips; ++j, left -= LANES, kd = dadd(kd, (double)LANES)) {
         float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
         if (left > 0 && !(ET && done)) {
           double p0[3];
@@ -403,6 +410,14 @@ __global__ void __launch_bounds__(kThreads, ISC_FAST_MINB) march_fast_kernel(con
         // Only the even lane's accumulator is used (it writes the pixel), so
         // it takes the odd lane's sample with a shuffle-down and composites
         // even-over-odd; the odd lane's accumulator is dead.
+        if constexpr (LANES == 4) {
+          // stations k..k+3 sit in parities 0..3 (lanes q, q+8, q+16, q+24):
+          // (s0 over s1) over (s2 over s3), then onto the pixel
+          c = over4(c, shfl_down_n(c, 8));
+          c = over4(c, shfl_down_n(c, 16));
+          acc = over4(acc, c);
+          continue;
+        }
         const float4 odd = shfl_down16(c);
         if constexpr (!ET) {
           acc = over4(acc, over4(c, odd));
@@ -592,7 +607,7 @@ static bool fast_eligible(const isc_render_args* a, FastField& F) {
 
 
 template <bool INTERP, bool GUARDED, bool PAIRED, int LINE = 0, int DIM = 1, bool ET = false,
-          typename T = float, bool AOS3 = false>
+          typename T = float, bool AOS3 = false, int LANES = 2>
 static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_t st) {
   static const int tw_env = getenv("ISC_TILE_W") ? __builtin_ctz(atoi(getenv("ISC_TILE_W"))) : -1;
   static const int cap_env = getenv("ISC_CTAS_PER_SM") ? atoi(getenv("ISC_CTAS_PER_SM")) : 0;
@@ -613,11 +628,12 @@ static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_
   OccupancyTuner::Choice ch{cap_env, tw_env >= 0 ? tw_env : 3};
   if (!cap_env && tw_env < 0 && !no_tune && PAIRED) {
     const int variant = (INTERP ? 1 : 0) | (GUARDED ? 2 : 0) | (ET ? 8 : 0) | (DIM << 4) | ((int)sizeof(T) << 8) |
-                        (LINE << 12) | (AOS3 ? 1 << 16 : 0);
+                        (LINE << 12) | (AOS3 ? 1 << 16 : 0) | (LANES << 17);
     ch = tuner().choose(OccupancyTuner::make_key(a, variant), st, &ev0, &ev1);
   }
-  const int tw_log2 = ch.tw_log2;
-  const int tw = 1 << tw_log2, th = (PAIRED ? 16 : 32) >> tw_log2;
+  // 4 lanes per ray: 8 rays per warp, the tile half as wide (8x2 -> 4x2)
+  const int tw_log2 = LANES == 4 ? max(ch.tw_log2 - 1, 0) : ch.tw_log2;
+  const int tw = 1 << tw_log2, th = (PAIRED ? 32 / LANES : 32) >> tw_log2;
   int tiles_x = (a->camera.width + tw - 1) / tw, tiles_y = (a->camera.height + th - 1) / th;
   int tile_x0 = 0, tile_y0 = 0;
   if (culled) {
@@ -633,14 +649,14 @@ static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_
   ISC_CUDA_CHECK(cudaGetDevice(&dev));
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm,
-                                                march_fast_kernel<INTERP, GUARDED, PAIRED, LINE, DIM, ET, T, AOS3>,
+                                                march_fast_kernel<INTERP, GUARDED, PAIRED, LINE, DIM, ET, T, AOS3, LANES>,
                                                 kThreads, 0);
   if (ch.cap > 0 && per_sm > ch.cap) per_sm = ch.cap;
   int grid = sms * (per_sm > 0 ? per_sm : 1);
   const int need = (n_codes + (kThreads / 32) - 1) / (kThreads / 32);  // one tile per warp at most
   if (grid > need) grid = need > 0 ? need : 1;
   if (ev0) cudaEventRecord(ev0, st);
-  march_fast_kernel<INTERP, GUARDED, PAIRED, LINE, DIM, ET, T, AOS3><<<grid, kThreads, 0, st>>>(
+  march_fast_kernel<INTERP, GUARDED, PAIRED, LINE, DIM, ET, T, AOS3, LANES><<<grid, kThreads, 0, st>>>(
       *a, F, tiles_x, tiles_y, super_x, n_codes, row_order ? 1 : 0, tw_log2, tile_x0, tile_y0);
   ISC_CUDA_CHECK(cudaGetLastError());
   if (ev1) cudaEventRecord(ev1, st);
@@ -654,8 +670,28 @@ int launch_staged(int lines, const isc_render_args* a, const FastField& F, cudaS
 // Guarded trilinear paired march with the analytic transfer function of
 // `lines` pieces when this instantiation covers it (lines <= MAXL), else the
 // shared-memory LUT.  MAXL bounds the template instantiations per variant.
+// A small frame: fewer 8x2-ray tiles in the image than two per resident
+// warp of the paired march (e.g. 256x256).  Decided on the image alone (not
+// the brick's screen rectangle), so a frame's compositing order -- and its
+// bits -- do not depend on debug outputs or on the decomposition.
+static bool small_frame(const isc_render_args* a) {
+  const char* q = getenv("ISC_QUAD");  // A/B, read per call: 0 off, 1 always
+  if (q) return atoi(q) == 1;
+  if (a->ray_dirs) return false;
+  const long long tiles = (long long)((a->camera.width + 7) / 8) * ((a->camera.height + 1) / 2);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return tiles < 2LL * sms * ISC_FAST_MINB * (kThreads / 32);
+}
+
 template <int MAXL, int DIM, bool ET, typename T, bool AOS3 = false>
 static int launch_line(int lines, const isc_render_args* a, const FastField& F, cudaStream_t st) {
+  if constexpr (DIM == 1 && !ET && !AOS3 && std::is_same<T, float>::value) {
+    if ((lines == 0 || lines == 1) && small_frame(a))
+      return lines ? launch_fast<true, true, true, 1, 1, false, float, false, 4>(a, F, st)
+                   : launch_fast<true, true, true, 0, 1, false, float, false, 4>(a, F, st);
+  }
   // 4..ISC_MAX_LUT_KINKS kinks: one variant with the count read at run time
   if constexpr (MAXL >= 4)
     if (lines > 4 && lines <= kLineRuntime) return launch_fast<true, true, true, kLineRuntime, DIM, ET, T, AOS3>(a, F, st);

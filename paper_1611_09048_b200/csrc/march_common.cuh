@@ -246,6 +246,12 @@ __device__ __forceinline__ int morton3(int w, int shift) {
   return ((w >> shift) & 1) | (((w >> (shift + 2)) & 1) << 1) | (((w >> (shift + 4)) & 1) << 2);
 }
 
+// Lane l receives lane l + n's value (full mask; lanes past 31 - n keep their own).
+__device__ __forceinline__ float4 shfl_down_n(float4 v, int n) {
+  return make_float4(__shfl_down_sync(0xffffffffu, v.x, n), __shfl_down_sync(0xffffffffu, v.y, n),
+                     __shfl_down_sync(0xffffffffu, v.z, n), __shfl_down_sync(0xffffffffu, v.w, n));
+}
+
 // Lanes 0-15 receive lane + 16's value (full mask; lanes 16-31 get their own).
 __device__ __forceinline__ float4 shfl_down16(float4 v) {
   return make_float4(__shfl_down_sync(0xffffffffu, v.x, 16), __shfl_down_sync(0xffffffffu, v.y, 16),

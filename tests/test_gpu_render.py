@@ -721,6 +721,7 @@ def test_staged_gather_is_bit_identical(seed, monkeypatch):
     overflows the warp's slice (far camera / long rays fall back to global)."""
     import paper_1611_09048_b200 as P
     torch = _torch()
+    monkeypatch.setenv("ISC_QUAD", "0")    # the staging prototype is the 2-lanes-per-ray march
     rng = np.random.default_rng(900 + seed)
     n = int(rng.choice([24, 48, 96]))
     field = torch.from_numpy(rng.random((n + 2,) * 3).astype(np.float32)).cuda()
