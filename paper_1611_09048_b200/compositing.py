@@ -164,12 +164,20 @@ def _wire(rnd, sender, lo, hi, body: bytes) -> bytes:
     return CompositeMessage.HEADER.pack(rnd, sender, lo, hi - lo) + body
 
 
+def _torch():
+    import torch
+    return torch
+
+
 def binary_swap(transport, local_pixels, order: Sequence[int], *, ops: Optional[DeviceOps] = None):
     """Composite every rank's image; the full frame appears on rank 0
     (returned as a new (H, W, 4) float32 CUDA tensor), ``None`` elsewhere."""
     from .transport import NvlinkTransport
     if isinstance(transport, NvlinkTransport):
         return _swap_nvlink(transport, local_pixels, list(order))
+    if transport.size == 1 and ops is None and getattr(local_pixels, "is_cuda", False) \
+            and local_pixels.dtype == _torch().float32 and local_pixels.shape[-1] == 4:
+        return local_pixels.clone(memory_format=_torch().contiguous_format)   # one rank: a copy (compositing.py:123)
     ops = ops or DeviceOps()
     shape = tuple(local_pixels.shape)
     flat = ops.as_flat(local_pixels)

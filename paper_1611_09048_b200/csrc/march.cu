@@ -645,12 +645,8 @@ static int launch_fast(const isc_render_args* a, const FastField& F, cudaStream_
   const int super_x = (tiles_x + 7) / 8, super_y = (tiles_y + 7) / 8;
   static const bool row_order = getenv("ISC_TILE_ROWS") != nullptr;
   const int n_codes = row_order ? tiles_x * tiles_y : super_x * super_y * 64;
-  int dev = 0, sms = 148, per_sm = 1;
-  ISC_CUDA_CHECK(cudaGetDevice(&dev));
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm,
-                                                march_fast_kernel<INTERP, GUARDED, PAIRED, LINE, DIM, ET, T, AOS3, LANES>,
-                                                kThreads, 0);
+  const int sms = cached_sm_count();
+  int per_sm = cached_blocks_per_sm<march_fast_kernel<INTERP, GUARDED, PAIRED, LINE, DIM, ET, T, AOS3, LANES>>(kThreads);
   if (ch.cap > 0 && per_sm > ch.cap) per_sm = ch.cap;
   int grid = sms * (per_sm > 0 ? per_sm : 1);
   const int need = (n_codes + (kThreads / 32) - 1) / (kThreads / 32);  // one tile per warp at most
@@ -679,10 +675,7 @@ static bool small_frame(const isc_render_args* a) {
   if (q) return atoi(q) == 1;
   if (a->ray_dirs) return false;
   const long long tiles = (long long)((a->camera.width + 7) / 8) * ((a->camera.height + 1) / 2);
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return tiles < 2LL * sms * ISC_FAST_MINB * (kThreads / 32);
+  return tiles < 2LL * cached_sm_count() * ISC_FAST_MINB * (kThreads / 32);
 }
 
 template <int MAXL, int DIM, bool ET, typename T, bool AOS3 = false>

@@ -236,6 +236,37 @@ inline bool brick_screen_rect(const isc_render_args* a, int& x0, int& y0, int& x
   return true;
 }
 
+// Host: resident CTAs per SM of `kernel` at `threads` threads and no dynamic
+// shared memory, queried once per (kernel, device) -- the occupancy query
+// costs microseconds on every frame otherwise.
+template <auto Kernel>
+inline int cached_blocks_per_sm(int threads) {
+  static int cache[64] = {};  // one per kernel instantiation (Kernel is a template argument)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (cache[dev] == 0) {
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, Kernel, threads, 0);
+    cache[dev] = n > 0 ? n : 1;
+  }
+  return cache[dev];
+}
+
+// Host: SM count of the current device (cached per device).
+inline int cached_sm_count() {
+  static int cache[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (cache[dev] == 0) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 148;
+  }
+  return cache[dev];
+}
+
 // The culled rectangle is the whole image: the kernel writes every pixel, so
 // the canvas needs no clearing first.
 inline bool rect_is_whole(const isc_render_args* a, int x0, int y0, int x1, int y1) {

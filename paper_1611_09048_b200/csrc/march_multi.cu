@@ -1002,10 +1002,13 @@ bool launch_iso_probe(const isc_render_args* a, cudaStream_t st, int* status) {
   const int n_codes = super_x * super_y * 64;
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  sms = cached_sm_count();
   auto kern = contig ? (s.n_steps ? iso_probe_kernel<true, true> : iso_probe_kernel<true, false>)
                      : (s.n_steps ? iso_probe_kernel<false, true> : iso_probe_kernel<false, false>);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, 0);
+  per_sm = contig ? (s.n_steps ? cached_blocks_per_sm<iso_probe_kernel<true, true>>(kThreads)
+                               : cached_blocks_per_sm<iso_probe_kernel<true, false>>(kThreads))
+                  : (s.n_steps ? cached_blocks_per_sm<iso_probe_kernel<false, true>>(kThreads)
+                               : cached_blocks_per_sm<iso_probe_kernel<false, false>>(kThreads));
   int grid = sms * (per_sm > 0 ? per_sm : 1);
   const int need = (n_codes + (kThreads / 32) - 1) / (kThreads / 32);
   if (grid > need) grid = need > 0 ? need : 1;

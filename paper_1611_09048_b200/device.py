@@ -30,9 +30,18 @@ def require_cuda() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
-def stream_handle(stream=None) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return int(s.cuda_stream)
+_RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
+def stream_handle(stream=None, device_index=None) -> int:
+    """Raw cudaStream_t of ``stream`` (default: the current stream of
+    ``device_index`` / the current device) -- without building a Stream
+    object on the per-frame path."""
+    if stream is not None:
+        return int(stream.cuda_stream)
+    if _RAW_STREAM is not None:
+        return int(_RAW_STREAM(torch.cuda.current_device() if device_index is None else device_index))
+    return int(torch.cuda.current_stream().cuda_stream)
 
 
 def as_device_field(array, device: torch.device) -> torch.Tensor:

@@ -488,7 +488,8 @@ def render_local(rank_ctx, scene: SceneState, plans: Optional[Sequence[SourcePla
     args.work_counter = ptr(stats) + 16
     if events is not None:
         events[0].record(stream)
-    _abi.check(_abi.lib().isc_render_local(C.byref(args), C.c_void_p(stream_handle(stream))), "render_local")
+    _abi.check(_abi.lib().isc_render_local(C.byref(args), C.c_void_p(stream_handle(stream, device.index))),
+               "render_local")
     if events is not None:
         events[1].record(stream)
 
@@ -506,10 +507,11 @@ def render_local(rank_ctx, scene: SceneState, plans: Optional[Sequence[SourcePla
         _replay_stations(station_recorder, counts, kr)
     # tensors the launch reads (staged fields, LUTs) stay alive for the
     # allocator until this stream has passed the kernel
-    run_stream = stream if stream is not None else torch.cuda.current_stream()
-    for t in keep:
-        t.record_stream(run_stream)
-    keep.clear()
+    if keep:
+        run_stream = stream if stream is not None else torch.cuda.current_stream(device)
+        for t in keep:
+            t.record_stream(run_stream)
+        keep.clear()
     return img
 
 
