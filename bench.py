@@ -347,7 +347,7 @@ def run_b200(args):
     barrier()
     start.record(stream)
     for i in range(k):
-        step(evs[i], sevs[i])
+        step(evs[i], sevs[i] if world > 1 else None)   # swap timing only where there is a swap
     end.record(stream)
     torch.cuda.synchronize()
     gc.enable()
@@ -356,7 +356,7 @@ def run_b200(args):
         transport.flush()             # a timed-out swap raises here
     ms_total = start.elapsed_time(end)
     kernel_ms = sum(a.elapsed_time(b) for a, b in evs) / k
-    swap_ms = sum(a.elapsed_time(b) for a, b in sevs) / k
+    swap_ms = sum(a.elapsed_time(b) for a, b in sevs) / k if world > 1 else 0.0
     t = torch.tensor([ms_total, kernel_ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
