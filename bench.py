@@ -433,7 +433,7 @@ def run_b200(args):
             dist.all_reduce(tl, op=dist.ReduceOp.MAX)
         return {"value": round(1000.0 / float(tl[0]), 3), "unit": "frames/s", "kernel_ms": round(float(tl[1]), 4),
                 "roofline_frac": round(float(bytes_v.item()) / (float(tl[1]) * 1e-3) / 1e9 / world / peak, 4),
-                "kernel": describe_kernel(plans_v, scene_v.settings, analytic)}
+                "kernel": describe_kernel(plans_v, scene_v.settings, analytic, scene_v.camera.image_size)}
 
     lut_path = tf_variants = tf4_variants = et_variant = None
     if len(scenes) == 1 and len(active) == 1:
@@ -517,7 +517,7 @@ def run_b200(args):
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic, "l1tex": l1tex,
                          "peak_source": peak_src,
-                         "kernel": describe_kernel(plans[0], scenes[0].settings), "kernel_ms": round(kernel_ms_max, 4),
+                         "kernel": describe_kernel(plans[0], scenes[0].settings, image_size=scenes[0].camera.image_size), "kernel_ms": round(kernel_ms_max, 4),
                          "algorithmic_bytes_per_launch": int(br.item() / world)},
             "e2e": e2e,
             "classification": ("analytic transfer function (exact: the LUT lerp is piecewise linear with "

@@ -397,7 +397,21 @@ def _aos3(arr) -> bool:
         return False
 
 
-def describe_kernel(plans: Sequence[SourcePlan], settings, analytic_lut: bool = True) -> str:
+def _small_frame(image_size) -> bool:
+    """march.cu small_frame: fewer 8x2 tiles than two per resident warp (4 CTAs
+    of 8 warps per SM) -> 4 lanes per ray.  ISC_QUAD=0/1 forces it."""
+    env = os.environ.get("ISC_QUAD")
+    if env is not None:
+        return env.strip() == "1"
+    if image_size is None:
+        return False
+    import torch as _t
+    w, h = image_size
+    sms = _t.cuda.get_device_properties(_t.cuda.current_device()).multi_processor_count
+    return ((w + 7) // 8) * ((h + 1) // 2) < 2 * sms * 4 * 8
+
+
+def describe_kernel(plans: Sequence[SourcePlan], settings, analytic_lut: bool = True, image_size=None) -> str:
     """Name of the march kernel ``isc_render_local`` dispatches to for these
     plans (mirrors the library's dispatch; for reports and bench lines)."""
     import torch as _t
@@ -418,8 +432,10 @@ def describe_kernel(plans: Sequence[SourcePlan], settings, analytic_lut: bool = 
             if pw is not None and guarded:
                 line = _line_variant(len(pw[2]), elem, dim, bool(et))
             aos3 = ",AOS3=1" if dim == 3 and _aos3(arr) else ""
+            lanes = ",LANES=4" if (guarded and elem == "float" and dim == 1 and not et and line in (0, 1)
+                                   and _small_frame(image_size)) else ""
             return (f"isc::march_fast_kernel<INTERP={int(interp)},GUARDED={int(guarded)},PAIRED=1,"
-                    f"LINE={line},DIM={dim},ET={int(et)},T={elem}{aos3}>")
+                    f"LINE={line},DIM={dim},ET={int(et)},T={elem}{aos3}{lanes}>")
     if (len(plans) == 2 and interp and not et and plans[0].mode == ISO_MODE and plans[1].mode != ISO_MODE
             and plans[0].handle.descriptor.feature_dim == 1 and plans[1].handle.descriptor.feature_dim in (1, 3)
             and all(p.handle.descriptor.has_guard for p in plans)

@@ -89,7 +89,8 @@ def main():
     torch.cuda.synchronize()
     ms = sorted(a.elapsed_time(b) for a, b in evs)
     res = {"lib": os.environ.get("ISC_LIB_PATH", "default"), "config": args.config, "alpha": args.alpha,
-           "kernel": describe_kernel(plans, scene.settings, analytic_lut=not args.lut),
+           "kernel": describe_kernel(plans, scene.settings, analytic_lut=not args.lut,
+                                     image_size=scene.camera.image_size),
            "dtype": args.dtype,
            "median_ms": round(ms[len(ms) // 2], 4),
            "min_ms": round(ms[0], 4), "stations": int(img.stations)}
