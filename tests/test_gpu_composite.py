@@ -72,8 +72,8 @@ def _over_np(front, back):
     return front + (np.float32(1.0) - front[:, 3:4]) * back
 
 
-@pytest.mark.parametrize("order", [[0, 1], [1, 0]])
-def test_swap_needs_no_coresident_grid(order):
+@pytest.mark.parametrize("order,hog", [([0, 1], False), ([1, 0], False), ([0, 1], True)])
+def test_swap_needs_no_coresident_grid(order, hog):
     """The swap kernel must make progress with any subset of its CTAs
     resident (in situ the simulation's kernels share the GPU, and CTAs are
     only guaranteed to run eventually, not together).  Rank 0 runs the real
@@ -83,7 +83,10 @@ def test_swap_needs_no_coresident_grid(order):
     independent of this GPU's SM residency, as on a multi-GPU box.  Arenas
     live in pinned host memory (device-accessible under unified
     addressing).  A design with a grid-wide barrier deadlocks here; the
-    per-slice protocol completes and matches the composite."""
+    per-slice protocol completes and matches the composite.  With ``hog``, a
+    stand-in for the simulation's kernels (isc_debug_occupy: one 1024-thread
+    CTA on half the SMs, spinning 0.3 s) holds the GPU from another stream
+    when the swap is launched."""
     import ctypes as C
     import threading
     import time
@@ -144,10 +147,16 @@ def test_swap_needs_no_coresident_grid(order):
             failure.append(exc)
 
     stream = torch.cuda.Stream()
+    hog_stream = torch.cuda.Stream()
+    if hog:
+        sms = lib.isc_device_sm_count(torch.cuda.current_device())
+        _abi.check(lib.isc_debug_occupy(max(sms // 2, 1), 1024, int(3e8), C.c_void_p(hog_stream.cuda_stream)),
+                   "occupy")
     t = threading.Thread(target=partner, daemon=True)
     t.start()
     _abi.check(lib.isc_binary_swap(C.byref(args), C.c_void_p(stream.cuda_stream)), "binary_swap")
     stream.synchronize()
+    hog_stream.synchronize()
     t.join(90)
     assert not failure, failure
     assert int(fa[_abi.ERR_WORD]) == 0, "rank 0 timed out waiting"
