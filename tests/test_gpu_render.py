@@ -247,6 +247,20 @@ def test_value_range_bit_exact():
         lo, hi = P.value_range(h, dom, ch)
         want = O.value_range(arr, 1, O.parse_steps(chain, dim))
         assert np.float32(lo) == want[0] and np.float32(hi) == want[1], chain
+    # contiguous float32 rows take 16-byte loads: long rows (several partial
+    # batches), a base pointer 4 bytes off 16-byte alignment, extremes placed
+    # in the scalar head and tail of a row
+    for width, off in ((300, 1), (1030, 0), (1030, 3), (7, 2)):
+        big = torch.from_numpy(rng.standard_normal((6, 5, width + 2 + off)).astype(np.float32)).cuda()
+        view = big[:, :, off:]                      # rows start `off` floats into the allocation
+        view[2, 3, 1] = 50.0                        # first interior element of a row (head)
+        view[4, 2, width] = -60.0                   # last interior element of a row (tail)
+        dom = P.LocalDomain((0, 0, 0), (width, 3, 4), 1)
+        h = P.array_backed_handle(P.SourceDescriptor("v", 1, has_guard=True), view, 1)
+        lo, hi = P.value_range(h, dom, P.parse_chain("", P.default_registry(), input_dim=1))
+        want = O.value_range(view.cpu().numpy(), 1, ())
+        assert np.float32(lo) == want[0] == np.float32(-60.0) and np.float32(hi) == want[1] == np.float32(50.0), \
+            (width, off)
 
 
 def test_kernel_nan_pow_chain_is_transparent():
