@@ -323,3 +323,25 @@ def test_multi_rank_frame_graph_replays(world):
     assert out.returncode == 0, out.stderr[-3000:]
     res = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
     assert res["all_identical"] and res["checks"] == 7 and res["nonzero"] > 0, res
+
+
+def test_nccl_backed_paths_world_one():
+    """The NCCL-default-group code paths of a multi-GPU run, exercised at world
+    size 1 on this GPU (NCCL needs one GPU per rank): the MIN/MAX all-reduce of
+    the auto value range on device tensors, the gloo side group of
+    TorchDistTransport under NCCL, the IPC arena exchange and binary_swap."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    helper = os.path.join(os.path.dirname(os.path.abspath(__file__)), "helpers", "nccl_paths.py")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+           "--master-addr=127.0.0.1", f"--master-port={port}", helper]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-3000:]
+    res = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert res["local"] == res["reduced"] and res["empty_is_nan"] and res["swap_equal"], res
