@@ -518,7 +518,13 @@ def run_b200(args):
                          "frac": round(achieved / peak, 4), "traffic": traffic, "l1tex": l1tex,
                          "peak_source": peak_src,
                          "kernel": describe_kernel(plans[0], scenes[0].settings, image_size=scenes[0].camera.image_size), "kernel_ms": round(kernel_ms_max, 4),
-                         "algorithmic_bytes_per_launch": int(br.item() / world)},
+                         "algorithmic_bytes_per_launch": int(br.item() / world),
+                         **({"frac_above_1": (
+                             "the 32 B/sample model counts every corner read; neighbouring rays share corners "
+                             "through L1 (hit rate %s), DRAM moved %s B per launch (ncu), so the kernel is not "
+                             "HBM-bound -- its limiter is %s" % (
+                                 l1tex and l1tex["l1_hit_rate"], traffic, l1tex and l1tex["limiter"]))}
+                            if achieved / peak > 1.0 else {})},
             "e2e": e2e,
             "classification": ("analytic transfer function (exact: the LUT lerp is piecewise linear with "
                                "few slope changes, raycast.lut_analytic); general shared-memory LUT path "
