@@ -269,14 +269,14 @@ __global__ void __launch_bounds__(kThreads) march_kernel(const __grid_constant__
 // station parities) or 4 for small frames (8 rays x 4 parities, merged by a
 // two-level shuffle tree): with fewer tiles than resident warps the launch
 // lasts as long as its longest ray, and 4 lanes halve that serial path.
-template <bool INTERP, bool GUARDED, bool PAIRED, int LINE = 0, int DIM = 1, bool ET = false,
-          typename T = float, bool AOS3 = false, int LANES = 2>
 // float3 sources: 3 CTAs per SM (<= 85 registers, no spills) -- C3's split
 // volume pass 1.518 -> 1.493 ms per frame; a float3-only volume render of the
 // same field 4.66 -> 4.71 ms (measured A/B)
 #ifndef ISC_FAST_MINB3
 #define ISC_FAST_MINB3 3
 #endif
+template <bool INTERP, bool GUARDED, bool PAIRED, int LINE = 0, int DIM = 1, bool ET = false,
+          typename T = float, bool AOS3 = false, int LANES = 2>
 __global__ void __launch_bounds__(kThreads, DIM == 3 ? ISC_FAST_MINB3 : ISC_FAST_MINB) march_fast_kernel(const __grid_constant__ isc_render_args a,
                                                               const FastField F, int tiles_x, int tiles_y,
                                                               int super_x, int n_codes, int row_order,
