@@ -131,3 +131,33 @@ def test_frame_graph_replay_matches_render():
     want2 = P.render_local(ctx, scene).pixels.cpu().numpy()
     got2 = g.replay().cpu().numpy()
     assert np.array_equal(got2, want2) and not np.array_equal(got2, got)
+
+
+def test_bench_json_line_contract():
+    """bench.py prints ONE JSON line with the driver's contract keys
+    (metric / value / unit / n_gpus / steps / warmup / ms_per_step /
+    higher_is_better / scaling / vs_baseline / dtype / data / config.workload,
+    roofline, e2e with copy byte counts, gpu_launches, clocks)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--config", "c1", "--steps", "3",
+                          "--warmup", "3", "--no-cpu-baseline", "--no-host-field-e2e"],
+                         capture_output=True, text=True, timeout=300, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1, lines
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks"):
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3 and d["higher_is_better"] is True
+    assert d["value"] > 0 and "workload" in d["config"]
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] and r["peak"] > 0
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] >= 3
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
