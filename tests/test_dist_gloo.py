@@ -152,3 +152,29 @@ def test_value_range_group_reduction(tmp_path, ranges, want):
             assert all(math.isnan(v) for v in got)
         else:
             assert got == want
+
+
+def test_bench_reference_arm_contract():
+    """`bench.py --impl reference` (runs on host cores, no GPU): one JSON line
+    with impl "reference", the metric / unit of the GPU arm, a cpu_baseline
+    naming what ran (the reference from baseline/_ref, else the oracle port)
+    and an e2e block with zero copy bytes; steps x ms_per_step is the timed
+    wall clock."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--steps", "2",
+                          "--warmup", "3", "--ref-step-s", "0.3"], capture_output=True, text=True, timeout=600,
+                         cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1, lines
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["unit"] == "frames/s" and d["higher_is_better"] is True
+    assert d["value"] > 0 and d["steps"] == 2
+    assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    c = d["consistency"]
+    assert abs(c["timed_seconds"] - c["steps_x_ms_per_step_s"]) <= 0.05 * c["timed_seconds"] + 0.01
